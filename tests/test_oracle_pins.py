@@ -1,0 +1,417 @@
+"""Pins for the CPU oracle: checks against what the paper and the mathematics fix,
+never against the oracle's own formula retyped.
+
+Each pin is chosen so that a plausible mistake (dropped term, wrong sign/index,
+transposed operand, wrong tie rule, wrong scale step) fails at least one test.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+def bf16_bits(vals):
+    """float values -> bf16 bit patterns via torch's RNE conversion (library routine)."""
+    t = torch.tensor(np.asarray(vals, dtype=np.float32)).to(torch.bfloat16)
+    return t.view(torch.int16).numpy().view(np.uint16).copy()
+
+
+def bf16_vals(bits):
+    return torch.from_numpy(np.asarray(bits, dtype=np.uint16).view(np.int16)).view(torch.bfloat16).float().numpy()
+
+
+# ---------------------------------------------------------------------------- formats
+
+def test_e4m3_decode_matches_torch_all_codes(orc):
+    """E4M3 decode of all 256 codes vs torch.float8_e4m3fn (independent library)."""
+    codes = torch.arange(256, dtype=torch.int32).to(torch.uint8)
+    ref = codes.view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    got = np.array([orc.e4m3_decode(c) for c in range(256)])
+    nan = np.isnan(ref)
+    assert np.array_equal(nan, np.isnan(got))
+    assert np.array_equal(ref[~nan], got[~nan])
+    assert orc.e4m3_decode(0x7E) == 448.0 and orc.e4m3_decode(0x01) == 2.0 ** -9
+
+
+def _neighbourhood(centres, ulps=3):
+    c = np.asarray(centres, dtype=np.float32)
+    bits = c.view(np.int32)
+    out = [c]
+    for d in range(1, ulps + 1):
+        out.append((bits + d).view(np.float32))
+        out.append((bits - d).view(np.float32))
+    v = np.concatenate(out)
+    return v[np.isfinite(v) & (v >= 0)]
+
+
+def test_e4m3_encode_matches_torch_rne(orc):
+    """Nearest-even E4M3 (R3) vs torch's RNE float->e4m3fn conversion on every
+    representable value and every midpoint +-3 ulp, plus random values; above the
+    RNE overflow point (464) torch gives NaN and satfinite gives 448."""
+    vals = np.array([orc.e4m3_decode(c) for c in range(0x7F)], dtype=np.float64)
+    mids = (vals[:-1] + vals[1:]) / 2
+    rng = np.random.default_rng(0)
+    probes = np.concatenate([
+        _neighbourhood(vals), _neighbourhood(mids),
+        np.exp(rng.uniform(np.log(1e-4), np.log(460), 20000)).astype(np.float32),
+    ])
+    probes = probes[probes <= 464.0]
+    ref = torch.from_numpy(probes).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    got = np.array([orc.e4m3_encode(float(v)) for v in probes], dtype=np.uint8)
+    assert np.array_equal(ref, got)
+    for big in (465.0, 1000.0, 3e38):
+        assert orc.e4m3_encode(big) == 0x7E
+
+
+def _e2m1_by_thresholds(v):
+    """Independent E2M1 cast: comparisons against the midpoints between the
+    representable magnitudes; at an exact midpoint take the even code."""
+    mags = GOLDEN["e2m1_magnitudes"]["values"]
+    a = abs(v)
+    code = 7
+    for i in range(7):
+        mid = (mags[i] + mags[i + 1]) / 2
+        if a < mid or (a == mid and i % 2 == 0):
+            code = i
+            break
+    return code | (8 if math.copysign(1.0, v) < 0 else 0)
+
+
+def test_e2m1_paper_examples(orc):
+    mags = GOLDEN["e2m1_magnitudes"]["values"]
+    # decode derived from the bit format (1 sign, 2 exponent, 1 mantissa; bias 1)
+    for nib in range(16):
+        e, m = (nib >> 1) & 3, nib & 1
+        mag = (m * 0.5) if e == 0 else (1 + m / 2) * 2.0 ** (e - 1)
+        assert orc.e2m1_decode(nib) == (-mag if nib & 8 else mag)
+        assert abs(orc.e2m1_decode(nib)) == mags[nib & 7]
+    for v, expect in GOLDEN["e2m1_cast_examples"]["cases"]:
+        c = orc.e2m1_encode(v)
+        assert orc.e2m1_decode(c) == expect and math.copysign(1, orc.e2m1_decode(c)) == math.copysign(1, expect)
+
+
+def test_e2m1_encode_matches_threshold_impl(orc):
+    mags = GOLDEN["e2m1_magnitudes"]["values"]
+    mids = [(mags[i] + mags[i + 1]) / 2 for i in range(7)]
+    rng = np.random.default_rng(1)
+    probes = np.concatenate([_neighbourhood(mags + mids, 4), rng.uniform(0, 8, 20000).astype(np.float32),
+                             np.float32([1e-30, 0.0, 6.0, 6.5, 1e30])])
+    probes = np.concatenate([probes, -probes])
+    for v in probes:
+        assert orc.e2m1_encode(float(v)) == _e2m1_by_thresholds(float(v)), v
+
+
+def test_bf16_rne_matches_torch(orc):
+    rng = np.random.default_rng(2)
+    bits = rng.integers(0, 2 ** 32, 200000, dtype=np.uint64).astype(np.uint32)
+    # ties: low 16 bits exactly 0x8000
+    bits[:5000] = (bits[:5000] & 0xFFFF0000) | 0x8000
+    f = bits.view(np.float32)
+    f = f[np.isfinite(f) & (np.abs(f) < 3.3e38)]
+    ref = bf16_bits(f)
+    got = np.array([orc.f32_to_bf16(float(v)) for v in f[:60000]], dtype=np.uint16)
+    assert np.array_equal(ref[:60000], got)
+
+
+# ---------------------------------------------------------------------------- NVFP4
+
+@pytest.mark.parametrize("div", [2688.0, 1344.0])
+def test_nvfp4_constant_block_paper_example(orc, div):
+    """16 copies of 3.0 -> every code is +6.0 and dequantizes to exactly 3.0;
+    holds for the tensor's own amax (2688) and the x2-headroom policy (1344)."""
+    v = GOLDEN["nvfp4_block_examples"]["const_block_value"]
+    x = bf16_bits(np.full((1, 16), v, np.float32))
+    g = orc.global_scale(v, div)
+    codes, sf = orc.nvfp4_quantize(x, g)
+    assert np.all(codes == 0x77)
+    assert np.all(orc.nvfp4_dequantize(codes, sf, g) == v)
+
+
+def test_nvfp4_zero_block(orc):
+    x = bf16_bits(np.zeros((2, 32), np.float32))
+    x[1, :] = 0x8000  # -0.0: sign kept (R5)
+    codes, sf = orc.nvfp4_quantize(x, 1.0)
+    assert np.all(sf == 0)
+    assert np.all(codes[0] == 0) and np.all(codes[1] == 0x88)
+    assert np.all(orc.nvfp4_dequantize(codes, sf, 1.0) == 0)
+
+
+def test_nvfp4_exact_representables_roundtrip(orc):
+    """A block whose values are E2M1 magnitudes times a power-of-two scale, with
+    the block max = 6*scale, quantizes to exactly those codes."""
+    rng = np.random.default_rng(3)
+    mags = np.array(GOLDEN["e2m1_magnitudes"]["values"])
+    for trial in range(50):
+        e = int(rng.integers(-8, 6))
+        idx = rng.integers(0, 8, 16)
+        idx[rng.integers(0, 16)] = 7
+        sign = rng.integers(0, 2, 16)
+        vals = np.where(sign == 1, -1, 1) * mags[idx] * 2.0 ** e
+        x = bf16_bits(vals[None, :].astype(np.float32))
+        codes, sf = orc.nvfp4_quantize(x, 1.0)
+        dq = orc.nvfp4_dequantize(codes, sf, 1.0)
+        assert np.array_equal(dq[0], vals)
+
+
+def test_nvfp4_error_bound_and_max_maps_to_six(orc):
+    """|x - x^| <= 1 * eff per element (half the widest E2M1 gap, 4..6), and each
+    non-zero block's largest element maps to magnitude 6."""
+    rng = np.random.default_rng(4)
+    x32 = (rng.standard_normal((8, 256)) * np.exp(rng.uniform(-3, 3, (8, 1)))).astype(np.float32)
+    x32[:, 7] *= 40
+    x = bf16_bits(x32)
+    xf = bf16_vals(x).astype(np.float64)
+    amax = float(np.abs(xf).max())
+    g = orc.global_scale(amax, 2688.0)
+    codes, sf = orc.nvfp4_quantize(x, g)
+    dq = orc.nvfp4_dequantize(codes, sf, g)
+    # eff = fl32(dec(s_b) * g), the effective block scale of Eq. 2
+    eff = (np.repeat(np.array([[orc.e4m3_decode(s) for s in row] for row in sf], dtype=np.float32), 16, axis=1)
+           * np.float32(g)).astype(np.float64)
+    assert np.all(np.abs(xf - dq) <= eff * (1 + 1e-6))
+    blocks = np.abs(dq).reshape(8, -1, 16).max(axis=2)
+    effb = eff.reshape(8, -1, 16)[:, :, 0]
+    assert np.all(blocks == 6 * effb)
+
+
+def test_nvfp4_reciprocal_reading_tie_vector(orc):
+    """Reading R4 pin: eff = 0.029296875 (E4M3 0x0F, g = 1), x = 1.25*eff.
+    x/eff would be the exact tie 1.25 -> 1.0, but x*fl(1/eff) = 1.2500001 -> 1.5."""
+    blk = np.zeros((1, 16), np.float32)
+    blk[0, 0] = 0.17578125          # 6 * eff -> block scale 0x0F
+    blk[0, 1] = 0.03662109375       # 1.25 * eff (exactly representable in bf16)
+    x = bf16_bits(blk)
+    assert bf16_vals(x)[0, 1] == np.float32(0.03662109375)
+    codes, sf = orc.nvfp4_quantize(x, 1.0)
+    assert sf[0, 0] == 0x0F
+    assert codes[0, 0] >> 4 == 3   # element 1 in the high nibble: code 1.5
+
+
+def test_sf_layout_is_a_bijection(orc):
+    m, k = 300, 320
+    sf = np.arange(m * (k // 16), dtype=np.int64).reshape(m, k // 16) % 251
+    sw = orc.sf_swizzle(sf.astype(np.uint8), m, k)
+    assert sw.size == 384 * 20
+    assert np.array_equal(orc.sf_unswizzle(sw, m, k), sf.astype(np.uint8))
+    offs = {orc.sf_offset(r, c, k) for r in range(m) for c in range(k // 16)}
+    assert len(offs) == m * (k // 16)
+
+
+# ---------------------------------------------------------------------------- INT8
+
+def test_int8_hand_example(orc):
+    """Per-token symmetric INT8: row [-2, 1, 0.5, 0]: s = 2/127; 1.0*127/2
+    = 63.5 exactly -> 64 (half to even); 0.5 -> 31.75 -> 32; -2 -> -127."""
+    x = bf16_bits(np.array([[-2.0, 1.0, 0.5, 0.0]], np.float32))
+    codes, s = orc.int8_quantize(x)
+    assert list(codes[0]) == [-127, 64, 32, 0]
+    assert s[0] == np.float32(2.0) / np.float32(127.0)
+    z, s0 = orc.int8_quantize(bf16_bits(np.zeros((1, 8), np.float32)))
+    assert s0[0] == 1.0 and np.all(z == 0)
+
+
+def test_int8_bound_and_extremum(orc):
+    rng = np.random.default_rng(5)
+    x32 = (rng.standard_normal((16, 192)) * np.exp(rng.uniform(-4, 4, (16, 1)))).astype(np.float32)
+    x = bf16_bits(x32)
+    xf = bf16_vals(x).astype(np.float64)
+    codes, s = orc.int8_quantize(x)
+    err = np.abs(xf - codes.astype(np.float64) * s[:, None].astype(np.float64))
+    assert np.all(err <= s[:, None] * (0.5 + 1e-5))
+    am = np.argmax(np.abs(xf), axis=1)
+    assert np.all(np.abs(codes[np.arange(16), am]) == 127)
+
+
+# ---------------------------------------------------------------------------- weights
+
+def test_pack_weights_consistency(orc):
+    rng = np.random.default_rng(6)
+    w = bf16_bits((rng.standard_normal((48, 128)) / np.sqrt(128)).astype(np.float32))
+    pk = orc.pack_weights(w)
+    amax = float(np.abs(bf16_vals(w)).max())
+    assert pk["fp4_g"] == orc.global_scale(amax, 2688.0)
+    c2, s2 = orc.nvfp4_quantize(w, pk["fp4_g"])
+    assert np.array_equal(c2, pk["fp4_codes"]) and np.array_equal(s2, pk["fp4_sf"])
+    # the INT8 form quantizes the DEQUANTIZED NVFP4 weights within s_w/2
+    what = orc.nvfp4_dequantize(pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"])
+    err = np.abs(what - pk["i8_codes"] * pk["i8_scale"][:, None].astype(np.float64))
+    assert np.all(err <= pk["i8_scale"][:, None] * (0.5 + 1e-5))
+    assert np.all(np.abs(pk["i8_codes"]).max(axis=1) == 127)
+
+
+# ---------------------------------------------------------------------------- GEMMs
+
+def test_gemm_int8_brute_force(orc):
+    rng = np.random.default_rng(7)
+    m, n, k = 5, 7, 64
+    a = rng.integers(-128, 128, (m, k)).astype(np.int8)
+    w = rng.integers(-128, 128, (n, k)).astype(np.int8)
+    sa = rng.uniform(0.001, 0.1, m).astype(np.float32)
+    sw = rng.uniform(0.001, 0.1, n).astype(np.float32)
+    b = rng.standard_normal(n).astype(np.float32)
+    acc, y = orc.gemm_int8(a, sa, w, sw, b)
+    for i in range(m):
+        for j in range(n):
+            exact = sum(int(a[i, t]) * int(w[j, t]) for t in range(k))
+            assert acc[i, j] == exact
+            yy = np.float32(np.float32(np.float32(exact) * sa[i]) * sw[j]) + b[j]
+            assert y[i, j] == np.float32(yy)
+    acc2, _ = orc.gemm_int8(a, sa, w, sw, b, rows=(2, 4))
+    assert np.array_equal(acc2, acc[2:4])
+
+
+def test_gemm_nvfp4_exact_fractions(orc):
+    rng = np.random.default_rng(8)
+    m, n, k = 3, 4, 64
+    ac = rng.integers(0, 256, (m, k // 2)).astype(np.uint8)
+    wc = rng.integers(0, 256, (n, k // 2)).astype(np.uint8)
+    asf = rng.integers(0x20, 0x50, (m, k // 16)).astype(np.uint8)
+    wsf = rng.integers(0x20, 0x50, (n, k // 16)).astype(np.uint8)
+    ga, gw = np.float32(0.37), np.float32(1.9)
+    b = rng.standard_normal(n).astype(np.float32)
+    y = orc.gemm_nvfp4(ac, asf, ga, wc, wsf, gw, b)
+
+    def dec(codes, sf, r, t):
+        byte = int(codes[r, t // 2])
+        nib = (byte >> 4) if t & 1 else (byte & 15)
+        return Fraction(orc.e2m1_decode(nib)) * Fraction(orc.e4m3_decode(int(sf[r, t // 16])))
+
+    gg = Fraction(float(np.float32(ga * gw)))
+    for i in range(m):
+        for j in range(n):
+            s = sum(dec(ac, asf, i, t) * dec(wc, wsf, j, t) for t in range(k))
+            exact = s * gg + Fraction(float(b[j]))
+            assert abs(Fraction(y[i, j]) - exact) <= abs(exact) * Fraction(1, 2 ** 50) + Fraction(1, 2 ** 80)
+
+
+def test_gemm_nvfp4_identity_weights(orc):
+    """W with one-hot rows of code +1.0 and unit block scales (0x38), g_w = 1:
+    Y = dequant(A) restricted to the selected columns (transposition check)."""
+    rng = np.random.default_rng(9)
+    m, k = 4, 32
+    x = bf16_bits(rng.standard_normal((m, k)).astype(np.float32))
+    ga = orc.global_scale(float(np.abs(bf16_vals(x)).max()), 2688.0)
+    ac, asf = orc.nvfp4_quantize(x, ga)
+    n = k
+    wc = np.zeros((n, k // 2), np.uint8)
+    for j in range(n):
+        wc[j, j // 2] = 0x02 << (4 * (j & 1))
+    wsf = np.full((n, k // 16), 0x38, np.uint8)
+    y = orc.gemm_nvfp4(ac, asf, ga, wc, wsf, 1.0, None)
+    # the block scales act inside the sum, g_a*g_w outside it (R3): Y = dec(a)*dec(sf_a)*g_a exactly
+    assert np.array_equal(y, orc.nvfp4_dequantize(ac, asf, 1.0) * float(ga))
+
+
+# ---------------------------------------------------------------------------- stats / TDC
+
+def test_block_stats_paper_examples(orc):
+    ones, twos = bf16_bits(np.ones(8, np.float32)), bf16_bits(2 * np.ones(8, np.float32))
+    _, st = orc.block_stats(ones, twos)
+    assert st[0] / st[1] == 1.0
+    _, st = orc.block_stats(bf16_bits([1, -1]), bf16_bits([1.5, -0.5]))
+    assert st[0] / st[1] == 0.5
+    d = bf16_bits([0.5, -1.0, 2.0, 0.25])
+    z = bf16_bits(np.zeros(4))
+    for dp, e in [(d, 0.0), (bf16_bits([-0.5, 1.0, -2.0, -0.25]), 2.0),
+                  (bf16_bits([2.0, 1.0, 0.0, 0.0]), 1.0), (bf16_bits([1.0, -2.0, 4.0, 0.5]), 0.0)]:
+        dn, st = orc.block_stats(z, d, dp)
+        assert np.array_equal(dn, d)
+        assert orc.cosine_error_from_stats(st[4], st[5], st[6]) == pytest.approx(e, abs=1e-15)
+
+
+def test_block_stats_vs_numpy(orc):
+    rng = np.random.default_rng(10)
+    xi = bf16_bits(rng.standard_normal(50000).astype(np.float32))
+    xo = bf16_bits((bf16_vals(xi) + 0.05 * rng.standard_normal(50000)).astype(np.float32))
+    dp = bf16_bits(0.05 * rng.standard_normal(50000).astype(np.float32))
+    dn, st = orc.block_stats(xi, xo, dp)
+    x, y, p = (bf16_vals(v).astype(np.float64) for v in (xi, xo, dp))
+    d = (bf16_vals(xo) - bf16_vals(xi)).astype(np.float32).astype(np.float64)
+    assert np.array_equal(dn, bf16_bits(d.astype(np.float32)))
+    n = bf16_vals(dn).astype(np.float64)
+    ref = [np.abs(d).sum(), np.abs(x).sum(), (d * d).sum(), (x * x).sum(), (n * p).sum(), (n * n).sum(), (p * p).sum()]
+    np.testing.assert_allclose(st, ref, rtol=1e-12)
+
+
+def test_tdc_skip_matches_torch_bf16_add(orc):
+    rng = np.random.default_rng(11)
+    xi = bf16_bits(rng.standard_normal(20000).astype(np.float32))
+    d = bf16_bits(0.1 * rng.standard_normal(20000).astype(np.float32))
+    out = orc.tdc_skip(xi, d)
+    ref = (torch.from_numpy(xi.view(np.int16)).view(torch.bfloat16) + torch.from_numpy(d.view(np.int16)).view(torch.bfloat16))
+    assert np.array_equal(out, ref.view(torch.int16).numpy().view(np.uint16))
+    assert np.array_equal(orc.tdc_skip(xi, bf16_bits(np.zeros(20000))), xi)
+
+
+# ---------------------------------------------------------------------------- decisions
+
+def test_threshold_and_routing_examples(orc):
+    g = GOLDEN["threshold_inversion"]
+    assert orc.derive_tau_gamma(g["alpha"], g["beta"], g["tau_rel"]) == pytest.approx(g["tau_gamma"], rel=1e-12)
+    assert orc.derive_tau_gamma(0.0, 0.001, 0.0025) == -math.inf
+    r = GOLDEN["routing_examples"]
+    for gamma, fmt in r["cases"]:
+        got = orc.route_block(gamma, [r["tau_gamma"]], t=5, prev_skipped=False)[0]
+        assert got == (orc.FMT_INT8 if fmt == "INT8" else orc.FMT_NVFP4)
+    assert orc.route_block(0.0, [0.015], t=0, prev_skipped=False) == [orc.FMT_INT8]
+    assert orc.route_block(0.0, [0.015], t=3, prev_skipped=True) == [orc.FMT_INT8]
+    assert orc.route_block(None, [0.015], t=3, prev_skipped=False) == [orc.FMT_INT8]
+    rng = np.random.default_rng(12)
+    for _ in range(1000):
+        a, b, tr = rng.uniform(0.01, 2), rng.uniform(-0.01, 0.01), rng.uniform(0, 0.05)
+        assert a * orc.derive_tau_gamma(a, b, tr) + b == pytest.approx(tr, abs=1e-15)
+
+
+def _run_trace(orc, cfg, etps, T):
+    st = orc.TdcState()
+    seq = []
+    for t in range(T):
+        dcs = orc.tdc_decide(st, cfg, t)
+        seq.append(dcs)
+        orc.tdc_update(st, cfg, t, dcs, etps[t] if dcs == 0 else None)
+    return seq, st
+
+
+def test_tdc_golden_trace(orc):
+    g = GOLDEN["tdc_golden_trace"]
+    cfg = orc.TdcConfig(rho=g["rho"], tau=g["tau"], n_max=g["n_max"])
+    st = orc.TdcState()
+    for t in range(2):   # warm-up computes
+        assert orc.tdc_decide(st, cfg, t) == 0
+        orc.tdc_update(st, cfg, t, 0, g["e_tp"])
+    accs = [st.e_acc]
+    decs = []
+    for t in range(2, 5):
+        d = orc.tdc_decide(st, cfg, t)
+        decs.append("SKIP" if d else "COMPUTE")
+        orc.tdc_update(st, cfg, t, d, g["e_tp"])
+        accs.append(st.e_acc)
+    assert decs == g["decisions_after_compute"]
+    assert accs[:3] == pytest.approx(g["e_acc_sequence"], rel=1e-12)
+
+
+def test_tdc_properties(orc):
+    rng = np.random.default_rng(13)
+    T = 50
+    # tau = 0 with e_tp > 0: never skips
+    seq, _ = _run_trace(orc, orc.TdcConfig(tau=0.0), rng.uniform(1e-6, 1e-2, T), T)
+    assert sum(seq) == 0
+    # tau = inf: exactly N_max skips between computes after warm-up
+    seq, _ = _run_trace(orc, orc.TdcConfig(tau=math.inf, n_max=2), rng.uniform(0, 1, T), T)
+    assert seq[:8] == [0, 0, 1, 1, 0, 1, 1, 0]
+    # never more than N_max consecutive skips
+    for trial in range(200):
+        n_max = int(rng.integers(1, 5))
+        seq, _ = _run_trace(orc, orc.TdcConfig(tau=float(rng.uniform(0, 0.01)), n_max=n_max),
+                            rng.uniform(0, 0.004, T), T)
+        run = best = 0
+        for s in seq:
+            run = run + 1 if s else 0
+            best = max(best, run)
+        assert best <= n_max
