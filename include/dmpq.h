@@ -1,0 +1,269 @@
+/*
+ * dmpq.h — C ABI of libdmpq: the B200 (sm_100a) hot path of 6Bit-Diffusion
+ * (arxiv 2603.18742): Dynamic Mixed-Precision Quantization (DMPQ, §4.1)
+ * and the Temporal Delta Cache (TDC, §4.2).
+ *
+ * Citations: P:<line> = PAPER.md line (the method's authority); Rn = reading n
+ * of DESIGN.md §3 (where the paper is silent or ambiguous).
+ *
+ * Conventions (all entry points)
+ *  - Every buffer is caller-owned. The library never allocates device memory and
+ *    never synchronises the device, except the host-pure helpers, which touch no
+ *    device state at all.
+ *  - Device work is enqueued on the caller's stream `s` (a cudaStream_t; NULL =
+ *    legacy default stream). Arguments are validated synchronously, before
+ *    anything is enqueued; a validation failure returns a status and enqueues
+ *    nothing. Device faults are asynchronous and surface at the caller's next
+ *    synchronisation.
+ *  - No exceptions cross the ABI. dmpq_last_error() describes the most recent
+ *    non-OK status of the calling thread.
+ *  - bf16 tensors are passed as `const uint16_t*` (their bit patterns), row
+ *    major. Device pointers must be 16-byte aligned and leading dimensions
+ *    multiples of 8 elements (DMPQ_EALIGN otherwise).
+ *  - Inputs must not alias outputs, except where stated (tdc_step SKIP).
+ *  - Stateless and re-entrant: calls on different streams may run concurrently.
+ */
+#ifndef DMPQ_H_
+#define DMPQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the ABI is the only exported surface of libdmpq */
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dmpq_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    DMPQ_OK = 0,
+    DMPQ_EINVAL = 1,       /* bad argument (NULL pointer, unknown enum, ...)      */
+    DMPQ_ESHAPE = 2,       /* unsupported or inconsistent dimensions              */
+    DMPQ_EALIGN = 3,       /* pointer / leading dimension alignment                */
+    DMPQ_EZERONORM = 4,    /* Eq. 3 undefined (||X||_1 == 0): routed INT8         */
+    DMPQ_ECUDA = 5,        /* a CUDA runtime call failed (launch, attribute, ...) */
+    DMPQ_EUNSUPPORTED = 6  /* no sm_100a device / feature not built               */
+} dmpq_status;
+
+/* Activation precision of one linear layer, Eq. 7. */
+typedef enum { DMPQ_FMT_INT8 = 0, DMPQ_FMT_NVFP4 = 1 } dmpq_fmt;
+
+const char* dmpq_last_error(void);
+const char* dmpq_version(void);
+
+/* ========================================================================== */
+/* Sizing helpers                                                             */
+/* ========================================================================== */
+
+/* Bytes of an NVFP4 block-scale buffer for a [rows x k] tensor in the device
+ * ("swizzled") layout consumed by the tcgen05 block-scaled MMA (R6): one E4M3
+ * byte per 16 elements, rows padded to a multiple of 128, scale columns to a
+ * multiple of 4, in 512-byte atoms of 128 rows x 4 scales, K-fastest. Byte of
+ * (row r, scale column c) = ((r/128)*(Kc/4) + c/4)*512 + (r%32)*16 +
+ * ((r%128)/32)*4 + c%4 with Kc = ceil(k/16 / 4)*4. */
+size_t dmpq_sf_bytes(int rows, int k);
+
+/* Workspace bytes tdc_step(REFRESH) needs for its deterministic two-stage
+ * reduction of an [m x h] tensor. */
+size_t tdc_workspace_bytes(int m, int h);
+
+/* ========================================================================== */
+/* Packed operands                                                            */
+/* ========================================================================== */
+
+/* Offline weight pack of one linear layer, P:184 ("all weights are quantized to
+ * NVFP4 offline"; INT8 weights for INT8-routed layers), reading R7: both forms
+ * are pre-packed; the INT8 form is the per-output-channel symmetric INT8
+ * quantization of the DEQUANTIZED NVFP4 weights. All pointers are device memory
+ * owned by the caller. */
+typedef struct {
+    int n, k;              /* out_features, in_features (nn.Linear W is [n x k]) */
+    uint8_t* fp4_codes;    /* [n x k/2]: E2M1 nibbles, element 2i in the low nibble */
+    uint8_t* fp4_sf;       /* dmpq_sf_bytes(n, k): E4M3 block scales, device layout */
+    float* fp4_g;          /* [1]: FP32 per-tensor scale g_w = max(amax/2688, FLT_MIN) */
+    int8_t* i8_codes;      /* [n x k] */
+    float* i8_scale;       /* [n]: per-output-channel scale */
+    const float* bias;     /* [n] or NULL (may point at caller memory) */
+} dmpq_weights;
+
+/* A quantized activation tensor, as written by dmpq_quantize_act. */
+typedef struct {
+    dmpq_fmt fmt;
+    int m, k;
+    void* codes;           /* NVFP4: uint8 [m x k/2]; INT8: int8 [m x k] (row-major, dense) */
+    uint8_t* sf;           /* NVFP4: dmpq_sf_bytes(m, k) block scales; INT8: unused */
+    const float* g;        /* NVFP4: device FP32 per-tensor scale g_a (input of the quantizer) */
+    float* row_scale;      /* INT8: [m] per-token scale s = amax_row/127 (R2) */
+} dmpq_act;
+
+/* ========================================================================== */
+/* 1. dmpq_pack_weights                                                       */
+/* ========================================================================== */
+
+/* Quantize W (bf16 [n x k], row stride k) into both packed forms (R7):
+ *   g_w = max(fl(amax(W)/2688), FLT_MIN);
+ *   NVFP4 codes/scales per Eq. 2 with that g (see dmpq_quantize_act);
+ *   W^ = fl(dec(code) * fl(dec(s_b) * g_w)),  s_w[n] = fl(max_k|W^|/127),
+ *   i8 = RNE(fl(W^ * fl(127/max_k|W^|)))   (s_w = 1, codes 0 for a zero row).
+ * `out` holds the caller's buffers; out->n, out->k must equal n, k.
+ * Shapes: k % 64 == 0, n % 16 == 0, n, k > 0. */
+dmpq_status dmpq_pack_weights(const uint16_t* W, int n, int k, dmpq_weights* out, dmpq_stream_t s);
+
+/* ========================================================================== */
+/* 2. dmpq_predict  (host-pure)                                               */
+/* ========================================================================== */
+
+/* Global (all ranks, all tokens) statistics of one block at the end of a step.
+ * The device writes them with tdc_step(REFRESH); the sums of Eq. 3 and Eq. 9. */
+typedef struct {
+    double sum_abs_d;  /* sum |Y - X|    (Eq. 3 numerator)   */
+    double sum_abs_x;  /* sum |X|        (Eq. 3 denominator) */
+    double sum_d2;     /* sum (Y - X)^2  (L2 variant, R1)     */
+    double sum_x2;     /* sum X^2                             */
+    double dot_dd;     /* sum Delta_t * Delta_prev  (Eq. 9)   */
+    double sum_dn2;    /* sum Delta_t^2                       */
+    double sum_dp2;    /* sum Delta_prev^2                    */
+} dmpq_block_stats;
+#define DMPQ_STATS_LEN 7
+
+typedef enum { DMPQ_GAMMA_L1 = 0, DMPQ_GAMMA_L2 = 1 } dmpq_gamma_metric;
+
+/* Eq. 6: tau_Gamma = (tau_rel - beta) / alpha; alpha <= eps_slope has no
+ * usable inversion and returns -INFINITY, which routes every Gamma to INT8. */
+double dmpq_derive_tau(double alpha, double beta, double tau_rel, double eps_slope);
+
+/* Routing of one block's n_layers linear layers for step t (Eq. 7):
+ *   Gamma_{t-1} = sum_abs_d / sum_abs_x  (Eq. 3; L2: sqrt(sum_d2)/sqrt(sum_x2)),
+ *   fmt_j = INT8  if t == 0 (no Gamma_{t-1}, R9) or prev_skipped (Gamma
+ *           missing after a Skip) or Gamma > tau_gamma[j];
+ *   fmt_j = NVFP4 otherwise (equality routes NVFP4).
+ * `st` is the block's statistics from step t-1 (ignored when t == 0 or
+ * prev_skipped). Writes fmt_out[0..n_layers) and *gamma_out (NAN if
+ * undefined). Returns DMPQ_EZERONORM, with every layer INT8, when the
+ * denominator is 0 and a Gamma was needed. */
+dmpq_status dmpq_predict(const dmpq_block_stats* st, const double* tau_gamma, int n_layers, int t,
+                         int prev_skipped, dmpq_gamma_metric metric, uint8_t* fmt_out, double* gamma_out);
+
+/* ========================================================================== */
+/* 3. dmpq_quantize_act                                                       */
+/* ========================================================================== */
+
+#define DMPQ_QF_LAYERNORM 1u  /* normalise each row first: h = (x - mean)/sqrt(var + eps), no affine (block glue) */
+#define DMPQ_QF_WRITE_H   2u  /* also store the bf16 values that were quantised into h_out */
+
+typedef struct {
+    uint32_t flags;
+    float ln_eps;          /* DMPQ_QF_LAYERNORM epsilon (e.g. 1e-6) */
+    uint16_t* h_out;       /* DMPQ_QF_WRITE_H: bf16 [m x k], row stride ldh */
+    int ldh;
+} dmpq_quant_opts;
+
+/* Online activation quantization of X (bf16 [m x k], row stride ldx) into one or
+ * both formats in a single HBM pass.
+ *  NVFP4 (Eq. 2, R3/R4), per row and 16-element block b:
+ *    a_b = max|x|; s_b = E4M3_rn_satfinite(fl(fl(a_b/6)/g)); eff = fl(dec(s_b)*g);
+ *    r = eff > 0 ? fl(1/eff) : 0; code = E2M1_rn_satfinite(fl(x*r)) (sign kept).
+ *    g is read from out_fp4->g (device FP32; the delayed policy of R3 sets it to
+ *    max(fl(amax_{t-1}/1344), FLT_MIN)). Scale rows in [m, ceil128(m)) are zeroed.
+ *  INT8 per token (R2): a = max_k|x|; s = fl(a/127); code =
+ *    RNE(fl(x*fl(127/a))); a == 0 gives s = 1 and zero codes.
+ *  Either output may be NULL, not both; out->m/k must equal m/k.
+ *  amax_out: if non-NULL, device FP32 that receives max(*amax_out, max|x|)
+ *  (atomic; the caller zeroes it once per step). With DMPQ_QF_LAYERNORM the
+ *  quantised (and amax'd) values are the bf16-rounded normalised rows.
+ *  Shapes: k % 64 == 0, 0 < k <= 16384, m >= 0 (m == 0 is a no-op). */
+dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
+                              dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s);
+
+/* Device-side global scale for the next NVFP4 quantization (R3):
+ * g_out[i] = max(fl(amax[i] / div), FLT_MIN) for i < count (div = 2688 for a
+ * tensor's own amax, 1344 for the delayed policy). */
+dmpq_status dmpq_global_scale(const float* amax, float div, float* g_out, int count, dmpq_stream_t s);
+
+/* ========================================================================== */
+/* 4. dmpq_gemm                                                               */
+/* ========================================================================== */
+
+#define DMPQ_EP_BIAS      1u  /* + bias[n] (W->bias)                                   */
+#define DMPQ_EP_GELU_TANH 2u  /* y = gelu_tanh(y)  (block glue)                        */
+#define DMPQ_EP_RESIDUAL  4u  /* y = residual[m,n] + gate[n] * y (gated residual glue) */
+
+typedef struct {
+    uint32_t flags;
+    const float* gate;         /* [n] (DMPQ_EP_RESIDUAL) */
+    const uint16_t* residual;  /* bf16 [m x n], row stride ldr (DMPQ_EP_RESIDUAL); may alias Y */
+    int ldr;
+} dmpq_epilogue;
+
+/* Y = A @ W^T with the dequant/bias epilogue (north_star), on tcgen05.
+ *  INT8  (kind::i8): acc = sum_k a*w exactly in int32 (TMEM);
+ *        y = fl(fl(fl(float(acc) * s_a[m]) * s_w[n]) + bias[n])        (R8)
+ *  NVFP4 (kind::mxf4nvf4.block_scale.scale_vec::4X): acc = sum_k
+ *        (dec(a)*s_a,b)(dec(w)*s_w,b) in the tensor core's FP32 accumulator;
+ *        y = fl(acc * fl(g_a*g_w)) + bias[n]
+ *  then the optional GELU / gated residual, stored as bf16 into Y (row stride
+ *  ldy) and/or as FP32 into Y32 (row stride n; NULL to skip). acc_or_null
+ *  (INT8 only) receives the raw int32 accumulators [m x n] (parity tests).
+ *  A->fmt selects the path and must match the packed operand used.
+ *  Shapes: A->k == W->k, k % 64 == 0, W->n % 32 == 0, m >= 0. */
+dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const dmpq_epilogue* ep,
+                      uint16_t* Y, int ldy, float* Y32, int32_t* acc_or_null, dmpq_stream_t s);
+
+/* ========================================================================== */
+/* 5. tdc_step  (+ host-pure TDC helpers)                                      */
+/* ========================================================================== */
+
+typedef enum { TDC_SKIP = 0, TDC_REFRESH = 1 } tdc_mode;
+typedef enum { TDC_COMPUTE = 0, TDC_DECIDE_SKIP = 1 } tdc_decision;
+
+/* Device part of TDC for one block (Eq. 8):
+ *  SKIP:    X_out = bf16(fl(X_in + Delta_{t_p}))  (X_out may alias X_in; Delta is
+ *           read from delta_cache; stats/workspace unused, may be NULL).
+ *  REFRESH: d = fl(X_out - X_in); Delta_new = bf16(d) overwrites delta_cache
+ *           (which held Delta_prev on entry); stats_out[0..7) receives, in FP64
+ *           (products exact in FP32, summed per 8-element vector in FP32, then
+ *           in FP64, fixed two-stage order: deterministic), the dmpq_block_stats
+ *           sums over the m x h elements. X_out is read-only here.
+ *  All tensors bf16 [m x h], dense (row stride h). workspace: device,
+ *  tdc_workspace_bytes(m, h). */
+dmpq_status tdc_step(tdc_mode mode, const uint16_t* X_in, uint16_t* X_out, uint16_t* delta_cache, int m, int h,
+                     double* stats_out, void* workspace, dmpq_stream_t s);
+
+/* Host-side per-block TDC state. */
+typedef struct {
+    int t_p;          /* last fully computed step (-1: none)           */
+    double e_tp;      /* E_{t_p}: prediction error measured at t_p     */
+    double e_acc;     /* E_acc                                         */
+    int last;         /* tdc_decision of the previous step (-1: none)  */
+    int n_computed;   /* computed deltas so far (warm-up needs two)    */
+} tdc_state;
+
+typedef struct {
+    double rho;       /* 0.001 */
+    double tau;       /* 0.003 */
+    int n_max;        /* 2     */
+} tdc_config;
+
+void tdc_init(tdc_state* st);
+
+/* Eq. 11: Skip iff e_acc <= tau and t - t_p <= n_max; the first two
+ * computes are forced (Eq. 9 needs two deltas, R10). */
+tdc_decision tdc_decide(const tdc_state* st, const tdc_config* cfg, int t);
+
+/* Eq. 10 at the end of step t. After a Compute, `st_global` holds the
+ * block's global statistics from tdc_step(REFRESH) and
+ * E_{t_p} = 1 - dot_dd / sqrt(sum_dn2 * sum_dp2) (Eq. 9; +INF when a norm
+ * is zero or this is the first compute); e_acc = E_{t_p}; t_p = t. After a
+ * Skip, e_acc = (e_acc + e_tp) + rho (st_global ignored, may be NULL). */
+void tdc_update(tdc_state* st, const tdc_config* cfg, int t, tdc_decision d, const dmpq_block_stats* st_global);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* DMPQ_H_ */

@@ -1,0 +1,299 @@
+// quant.cu — dmpq_quantize_act: online NVFP4 / per-token INT8 activation
+// quantization (Eq. 2; R2-R6), optionally
+// with a fused row LayerNorm prologue (block glue), and dmpq_global_scale.
+//
+// HBM-bound streaming kernel. Each row is held in registers by one warp (k <= 512)
+// or one CTA (k > 512): NV 16-byte vectors (8 bf16) per thread, loaded once,
+// coalesced (consecutive lanes own consecutive vectors). Reductions: warp
+// shuffles + shared memory, fixed order (deterministic). Per 16-element NVFP4
+// block the two lanes holding it exchange their maxima with one shuffle; four
+// consecutive blocks' E4M3 scales (one 32-bit word of the swizzled scale layout)
+// are gathered by shuffles and stored by one lane. Persistent grid over rows.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace dmpq {
+
+struct QuantParams {
+    const uint16_t* X;
+    int m, k, ldx;
+    uint32_t flags;
+    float ln_eps;
+    uint16_t* h_out;
+    int ldh;
+    int8_t* i8_codes;
+    float* i8_scale;
+    uint8_t* fp4_codes;
+    uint8_t* fp4_sf;
+    const float* g;
+    float* amax_out;
+    int kc4;     // scale-column atoms per 128-row tile: ceil(k/16/4)
+    int m_pad;   // rows rounded up to 128 (scale rows to zero-fill)
+};
+
+template <bool WARP_ROW>
+struct RowReduce {
+    float* red;  // shared scratch, >= 33 floats
+    __device__ __forceinline__ float sum(float v) {
+        v = warp_sum(v);
+        if constexpr (WARP_ROW) return v;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+        __syncthreads();
+        if (l == 0) red[w] = v;
+        __syncthreads();
+        float t = (l < nw) ? red[l] : 0.0f;
+        return warp_sum(t);
+    }
+    __device__ __forceinline__ float max(float v) {
+        v = warp_max(v);
+        if constexpr (WARP_ROW) return v;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+        __syncthreads();
+        if (l == 0) red[w] = v;
+        __syncthreads();
+        float t = (l < nw) ? red[l] : 0.0f;
+        return warp_max(t);
+    }
+};
+
+template <int NV, bool WARP_ROW>
+__global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
+    __shared__ float red[40];
+    RowReduce<WARP_ROW> rr{red};
+    const int lane = threadIdx.x & 31;
+    const int tpr = WARP_ROW ? 32 : blockDim.x;                 // threads per row
+    const int tid = WARP_ROW ? lane : threadIdx.x;
+    const int rows_per_cta = WARP_ROW ? (blockDim.x >> 5) : 1;
+    const int row_slot = WARP_ROW ? (threadIdx.x >> 5) : 0;
+    const int nvec = p.k >> 3;
+    const bool want_fp4 = p.fp4_codes != nullptr;
+    const bool want_i8 = p.i8_codes != nullptr;
+    const float g = want_fp4 ? *p.g : 1.0f;
+    float cta_amax = 0.0f;
+
+    for (int row = blockIdx.x * rows_per_cta + row_slot; row < p.m; row += gridDim.x * rows_per_cta) {
+        const uint16_t* xr = p.X + (size_t)row * p.ldx;
+        uint4 v[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int vi = tid + i * tpr;
+            v[i] = (vi < nvec) ? ldg_stream(xr + (size_t)vi * 8) : make_uint4(0, 0, 0, 0);
+        }
+        if (p.flags & DMPQ_QF_LAYERNORM) {
+            // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue)
+            float s = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) s = __fadd_rn(__fadd_rn(s, bf16lo(w[j])), bf16hi(w[j]));
+            }
+            const float mean = __fdiv_rn(rr.sum(s), (float)p.k);
+            float q = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                if (vi >= nvec) continue;
+                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float a = __fsub_rn(bf16lo(w[j]), mean), b = __fsub_rn(bf16hi(w[j]), mean);
+                    q = __fadd_rn(q, __fadd_rn(__fmul_rn(a, a), __fmul_rn(b, b)));
+                }
+            }
+            const float var = __fdiv_rn(rr.sum(q), (float)p.k);
+            const float rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps)));
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    w[j] = pack_bf16x2(__fmul_rn(__fsub_rn(bf16lo(w[j]), mean), rstd),
+                                       __fmul_rn(__fsub_rn(bf16hi(w[j]), mean), rstd));
+                v[i] = (vi < nvec) ? make_uint4(w[0], w[1], w[2], w[3]) : make_uint4(0, 0, 0, 0);
+                if ((p.flags & DMPQ_QF_WRITE_H) && vi < nvec)
+                    *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)vi * 8) = v[i];
+            }
+        }
+        // per-vector |x| maxima
+        float vmax[NV];
+        float tmax = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+            float mx = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mx = fmaxf(mx, fmaxf(fabsf(bf16lo(w[j])), fabsf(bf16hi(w[j]))));
+            vmax[i] = mx;
+            tmax = fmaxf(tmax, mx);
+        }
+        cta_amax = fmaxf(cta_amax, tmax);
+
+        if (want_fp4) {
+            const int rt = row >> 7;
+            uint8_t* sf_row = p.fp4_sf + (size_t)rt * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                // a_b: max over the 16-element block = this vector and its pair lane
+                const float a_b = fmaxf(vmax[i], __shfl_xor_sync(0xffffffffu, vmax[i], 1));
+                const float raw = __fdiv_rn(__fdiv_rn(a_b, 6.0f), g);
+                const uint32_t sb = e4m3_rn_satfinite(raw);
+                const float eff = __fmul_rn(e4m3_decode(sb), g);
+                const float rcp = eff > 0.0f ? __frcp_rn(eff) : 0.0f;
+                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+                uint32_t codes = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    codes |= e2m1x2(__fmul_rn(bf16lo(w[j]), rcp), __fmul_rn(bf16hi(w[j]), rcp)) << (8 * j);
+                // gather the 4 block scales of this 64-element group (lanes 8q, 8q+2, 8q+4, 8q+6)
+                const int base = lane & ~7;
+                const uint32_t s0 = __shfl_sync(0xffffffffu, sb, base + 0);
+                const uint32_t s1 = __shfl_sync(0xffffffffu, sb, base + 2);
+                const uint32_t s2 = __shfl_sync(0xffffffffu, sb, base + 4);
+                const uint32_t s3 = __shfl_sync(0xffffffffu, sb, base + 6);
+                if (vi < nvec) {
+                    *reinterpret_cast<uint32_t*>(p.fp4_codes + (size_t)row * (p.k >> 1) + (size_t)vi * 4) = codes;
+                    if ((lane & 7) == 0) {
+                        const int c4 = vi >> 3;  // scale-column atom (4 scales = 64 elements)
+                        *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+                    }
+                }
+            }
+        }
+        if (want_i8) {
+            const float a = rr.max(tmax);
+            const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
+            if (tid == 0) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+                uint32_t out[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t packed = 0;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const uint32_t ww = w[2 * h + j];
+                        int c0 = __float2int_rn(__fmul_rn(bf16lo(ww), rcp));
+                        int c1 = __float2int_rn(__fmul_rn(bf16hi(ww), rcp));
+                        c0 = max(-128, min(127, c0));
+                        c1 = max(-128, min(127, c1));
+                        packed |= ((uint32_t)(c0 & 0xFF) | ((uint32_t)(c1 & 0xFF) << 8)) << (16 * j);
+                    }
+                    out[h] = packed;
+                }
+                if (vi < nvec)
+                    *reinterpret_cast<uint2*>(p.i8_codes + (size_t)row * p.k + (size_t)vi * 8) = make_uint2(out[0], out[1]);
+            }
+        }
+    }
+    // zero the scale rows that pad m up to a multiple of 128 (read by the GEMM's M tail)
+    if (want_fp4) {
+        const int pad_rows = p.m_pad - p.m;
+        const int words_per_row = p.kc4;  // one 32-bit word per (row, atom)
+        for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < pad_rows * words_per_row;
+             idx += gridDim.x * blockDim.x) {
+            const int row = p.m + idx / words_per_row, c4 = idx % words_per_row;
+            uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
+            *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = 0u;
+        }
+    }
+    if (p.amax_out) {
+        float a = warp_max(cta_amax);
+        if (lane == 0) atomic_max_nonneg(p.amax_out, a);
+    }
+}
+
+__global__ void global_scale_kernel(const float* amax, float div, float* g_out, int count) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        float g = __fdiv_rn(amax[i], div);
+        g_out[i] = g < 1.17549435e-38f ? 1.17549435e-38f : g;
+    }
+}
+
+template <int NV, bool WR>
+static void launch_quant(const QuantParams& p, int threads, cudaStream_t s) {
+    int rows_per_cta = WR ? threads / 32 : 1;
+    int ctas_needed = (p.m + rows_per_cta - 1) / rows_per_cta;
+    int grid = num_sms() * (WR ? 8 : (2048 / threads));
+    if (grid > ctas_needed) grid = ctas_needed;
+    if (grid < 1) grid = 1;
+    quant_act_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
+}
+
+}  // namespace dmpq
+
+using namespace dmpq;
+
+extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
+                                         dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s) {
+    DMPQ_REQUIRE(out_i8 || out_fp4, DMPQ_EINVAL, "dmpq_quantize_act: both outputs are NULL");
+    DMPQ_REQUIRE(m >= 0 && k > 0 && k % 64 == 0 && k <= 16384, DMPQ_ESHAPE,
+                 "dmpq_quantize_act: need k %% 64 == 0, 0 < k <= 16384, m >= 0 (m=%d k=%d)", m, k);
+    DMPQ_REQUIRE(ldx >= k && ldx % 8 == 0, DMPQ_EALIGN, "dmpq_quantize_act: ldx=%d must be >= k and a multiple of 8", ldx);
+    DMPQ_REQUIRE(X && aligned16(X), DMPQ_EALIGN, "dmpq_quantize_act: X must be a 16-byte aligned device pointer");
+    if (out_i8) {
+        DMPQ_REQUIRE(out_i8->fmt == DMPQ_FMT_INT8 && out_i8->m == m && out_i8->k == k, DMPQ_ESHAPE,
+                     "dmpq_quantize_act: INT8 output descriptor mismatch");
+        DMPQ_REQUIRE(out_i8->codes && out_i8->row_scale && aligned16(out_i8->codes), DMPQ_EALIGN,
+                     "dmpq_quantize_act: INT8 output pointers");
+    }
+    if (out_fp4) {
+        DMPQ_REQUIRE(out_fp4->fmt == DMPQ_FMT_NVFP4 && out_fp4->m == m && out_fp4->k == k, DMPQ_ESHAPE,
+                     "dmpq_quantize_act: NVFP4 output descriptor mismatch");
+        DMPQ_REQUIRE(out_fp4->codes && out_fp4->sf && out_fp4->g && aligned16(out_fp4->codes) && aligned16(out_fp4->sf),
+                     DMPQ_EALIGN, "dmpq_quantize_act: NVFP4 output pointers");
+    }
+    QuantParams p{};
+    p.X = X; p.m = m; p.k = k; p.ldx = ldx;
+    p.flags = opts ? opts->flags : 0u;
+    p.ln_eps = opts ? opts->ln_eps : 0.0f;
+    if (p.flags & DMPQ_QF_WRITE_H) {
+        DMPQ_REQUIRE(opts->h_out && aligned16(opts->h_out) && opts->ldh >= k && opts->ldh % 8 == 0, DMPQ_EALIGN,
+                     "dmpq_quantize_act: h_out / ldh");
+        p.h_out = opts->h_out; p.ldh = opts->ldh;
+    }
+    p.i8_codes = out_i8 ? reinterpret_cast<int8_t*>(out_i8->codes) : nullptr;
+    p.i8_scale = out_i8 ? out_i8->row_scale : nullptr;
+    p.fp4_codes = out_fp4 ? reinterpret_cast<uint8_t*>(out_fp4->codes) : nullptr;
+    p.fp4_sf = out_fp4 ? out_fp4->sf : nullptr;
+    p.g = out_fp4 ? out_fp4->g : nullptr;
+    p.amax_out = amax_out;
+    p.kc4 = ((k / 16) + 3) / 4;
+    p.m_pad = (m + 127) / 128 * 128;
+    if (m == 0) return DMPQ_OK;
+    DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_quantize_act: needs an sm_100 device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+    const int nvec = k / 8;
+    if (nvec <= 64) {  // warp per row
+        if (nvec <= 32) launch_quant<1, true>(p, 256, st);
+        else launch_quant<2, true>(p, 256, st);
+    } else {
+        int nv = (nvec + 255) / 256;
+        int threads = ((nvec + nv - 1) / nv + 31) / 32 * 32;
+        switch (nv) {
+            case 1: launch_quant<1, false>(p, threads, st); break;
+            case 2: launch_quant<2, false>(p, threads, st); break;
+            case 3: launch_quant<3, false>(p, threads, st); break;
+            case 4: launch_quant<4, false>(p, threads, st); break;
+            case 5: launch_quant<5, false>(p, threads, st); break;
+            case 6: launch_quant<6, false>(p, threads, st); break;
+            case 7: launch_quant<7, false>(p, threads, st); break;
+            default: launch_quant<8, false>(p, threads, st); break;
+        }
+    }
+    return check_launch("dmpq_quantize_act");
+}
+
+extern "C" dmpq_status dmpq_global_scale(const float* amax, float div, float* g_out, int count, dmpq_stream_t s) {
+    DMPQ_REQUIRE(amax && g_out && count >= 0 && div > 0.0f, DMPQ_EINVAL, "dmpq_global_scale: bad arguments");
+    if (count == 0) return DMPQ_OK;
+    DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_global_scale: needs an sm_100 device");
+    global_scale_kernel<<<(count + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(s)>>>(amax, div, g_out, count);
+    return check_launch("dmpq_global_scale");
+}

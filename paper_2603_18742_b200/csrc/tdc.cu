@@ -1,0 +1,133 @@
+// tdc.cu — tdc_step: the device half of the Temporal Delta Cache (§4.2).
+//   SKIP:        X_out = bf16(fl(X_in + Delta_tp))
+//   REFRESH (Eq. 8): Delta_new = bf16(fl(X_out - X_in)) into the cache, fused
+//            with the FP64 statistics of Eq. 3 (Gamma) and Eq. 9 (cosine of the
+//            two most recent computed deltas).
+// HBM-bound streaming kernels: 16-byte vectors, persistent grid-stride loop.
+// Statistics: exact-ish FP32 sums over each 8-element vector, accumulated in FP64
+// per thread, reduced warp -> CTA in fixed order; per-CTA partials are summed in
+// CTA order by the last CTA to finish (deterministic for a given m x h).
+#include "common.cuh"
+
+namespace dmpq {
+
+constexpr int kTdcThreads = 256;
+constexpr int kTdcCtasPerSm = 4;
+
+static int tdc_grid(long long nvec) {
+    long long g = (long long)num_sms() * kTdcCtasPerSm;
+    long long need = (nvec + kTdcThreads - 1) / kTdcThreads;
+    if (g > need) g = need;
+    return (int)(g < 1 ? 1 : g);
+}
+
+__global__ void __launch_bounds__(kTdcThreads) tdc_skip_kernel(const uint16_t* x_in, const uint16_t* delta,
+                                                               uint16_t* x_out, long long nvec) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 x = ldg_stream(x_in + i * 8);
+        const uint4 d = ldg_stream(delta + i * 8);
+        const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, dw[4] = {d.x, d.y, d.z, d.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            o[j] = pack_bf16x2(__fadd_rn(bf16lo(xw[j]), bf16lo(dw[j])), __fadd_rn(bf16hi(xw[j]), bf16hi(dw[j])));
+        *reinterpret_cast<uint4*>(x_out + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+__global__ void __launch_bounds__(kTdcThreads) tdc_refresh_kernel(const uint16_t* __restrict__ x_in,
+                                                                  const uint16_t* __restrict__ x_out,
+                                                                  uint16_t* delta, long long nvec,
+                                                                  double* partials, unsigned int* counter,
+                                                                  double* stats_out) {
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 x = ldg_stream(x_in + i * 8);
+        const uint4 y = ldg_stream(x_out + i * 8);
+        const uint4 p = *reinterpret_cast<const uint4*>(delta + i * 8);
+        const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w}, pw[4] = {p.x, p.y, p.z, p.w};
+        float s[7] = {0, 0, 0, 0, 0, 0, 0};
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float xa = bf16lo(xw[j]), xb = bf16hi(xw[j]);
+            const float da = __fsub_rn(bf16lo(yw[j]), xa), db = __fsub_rn(bf16hi(yw[j]), xb);
+            o[j] = pack_bf16x2(da, db);
+            const float na = bf16lo(o[j]), nb = bf16hi(o[j]);
+            const float pa = bf16lo(pw[j]), pb = bf16hi(pw[j]);
+            s[0] = __fadd_rn(s[0], __fadd_rn(fabsf(da), fabsf(db)));
+            s[1] = __fadd_rn(s[1], __fadd_rn(fabsf(xa), fabsf(xb)));
+            s[2] = __fadd_rn(s[2], __fadd_rn(__fmul_rn(da, da), __fmul_rn(db, db)));
+            s[3] = __fadd_rn(s[3], __fadd_rn(__fmul_rn(xa, xa), __fmul_rn(xb, xb)));
+            s[4] = __fadd_rn(s[4], __fadd_rn(__fmul_rn(na, pa), __fmul_rn(nb, pb)));
+            s[5] = __fadd_rn(s[5], __fadd_rn(__fmul_rn(na, na), __fmul_rn(nb, nb)));
+            s[6] = __fadd_rn(s[6], __fadd_rn(__fmul_rn(pa, pa), __fmul_rn(pb, pb)));
+        }
+        *reinterpret_cast<uint4*>(delta + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+        for (int j = 0; j < 7; ++j) acc[j] = __dadd_rn(acc[j], (double)s[j]);
+    }
+    __shared__ double red[kTdcThreads / 32][7];
+    __shared__ bool is_last;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+        double v = warp_sum_d(acc[j]);
+        if (l == 0) red[w][j] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 7) {
+        double v = 0.0;
+        for (int ww = 0; ww < kTdcThreads / 32; ++ww) v = __dadd_rn(v, red[ww][threadIdx.x]);
+        partials[(size_t)blockIdx.x * 7 + threadIdx.x] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        if (threadIdx.x < 7) {
+            double v = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) v = __dadd_rn(v, __ldcg(partials + (size_t)b * 7 + threadIdx.x));
+            stats_out[threadIdx.x] = v;
+        }
+        if (threadIdx.x == 0) *counter = 0u;  // leave the workspace ready for the next call
+    }
+}
+
+}  // namespace dmpq
+
+using namespace dmpq;
+
+extern "C" size_t tdc_workspace_bytes(int m, int h) {
+    (void)m; (void)h;
+    // partials for the largest grid any device can use + the completion counter
+    return (size_t)1024 * kTdcCtasPerSm * 7 * sizeof(double) + 256;
+}
+
+extern "C" dmpq_status tdc_step(tdc_mode mode, const uint16_t* X_in, uint16_t* X_out, uint16_t* delta_cache, int m, int h,
+                                double* stats_out, void* workspace, dmpq_stream_t s) {
+    DMPQ_REQUIRE(mode == TDC_SKIP || mode == TDC_REFRESH, DMPQ_EINVAL, "tdc_step: unknown mode %d", (int)mode);
+    DMPQ_REQUIRE(m >= 0 && h > 0 && h % 8 == 0, DMPQ_ESHAPE, "tdc_step: need m >= 0, h %% 8 == 0 (m=%d h=%d)", m, h);
+    DMPQ_REQUIRE(X_in && X_out && delta_cache && aligned16(X_in) && aligned16(X_out) && aligned16(delta_cache),
+                 DMPQ_EALIGN, "tdc_step: tensors must be 16-byte aligned device pointers");
+    const long long nvec = (long long)m * h / 8;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+    if (mode == TDC_SKIP) {
+        if (nvec == 0) return DMPQ_OK;
+        DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "tdc_step: needs an sm_100 device");
+        tdc_skip_kernel<<<tdc_grid(nvec), kTdcThreads, 0, st>>>(X_in, delta_cache, X_out, nvec);
+        return check_launch("tdc_step(SKIP)");
+    }
+    DMPQ_REQUIRE(X_in != X_out, DMPQ_EINVAL, "tdc_step(REFRESH): X_out must not alias X_in");
+    DMPQ_REQUIRE(stats_out && workspace && aligned16(workspace), DMPQ_EINVAL, "tdc_step(REFRESH): stats_out/workspace");
+    DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "tdc_step: needs an sm_100 device");
+    const int grid = nvec == 0 ? 1 : tdc_grid(nvec);
+    DMPQ_REQUIRE(grid <= 1024 * kTdcCtasPerSm, DMPQ_EUNSUPPORTED, "tdc_step: grid too large for workspace");
+    double* partials = reinterpret_cast<double*>(workspace);
+    unsigned int* counter = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(workspace) +
+                                                            (size_t)1024 * kTdcCtasPerSm * 7 * sizeof(double));
+    tdc_refresh_kernel<<<grid, kTdcThreads, 0, st>>>(X_in, X_out, delta_cache, nvec, partials, counter, stats_out);
+    return check_launch("tdc_step(REFRESH)");
+}

@@ -1,0 +1,212 @@
+"""Python binding of libdmpq with the C ABI's names (include/dmpq.h).
+
+Argument marshalling only: torch supplies device memory and the current CUDA
+stream; every step of the hot path runs in libdmpq's sm_100a kernels. There is
+no CPU or eager-PyTorch fallback — a missing library or GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib as L
+
+__all__ = [
+    "PackedWeights", "QuantAct", "dmpq_pack_weights", "dmpq_predict", "dmpq_derive_tau", "dmpq_quantize_act",
+    "dmpq_global_scale", "dmpq_gemm", "tdc_step", "tdc_decide", "tdc_update", "tdc_new_state", "sf_bytes",
+    "tdc_workspace_bytes", "FMT_INT8", "FMT_NVFP4",
+]
+
+FMT_INT8, FMT_NVFP4 = L.FMT_INT8, L.FMT_NVFP4
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check_dev(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libdmpq has no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def sf_bytes(rows: int, k: int) -> int:
+    return int(L.lib().dmpq_sf_bytes(rows, k))
+
+
+def tdc_workspace_bytes(m: int, h: int) -> int:
+    return int(L.lib().tdc_workspace_bytes(m, h))
+
+
+# --------------------------------------------------------------------------- weights
+
+@dataclass
+class PackedWeights:
+    n: int
+    k: int
+    fp4_codes: torch.Tensor
+    fp4_sf: torch.Tensor
+    fp4_g: torch.Tensor
+    i8_codes: torch.Tensor
+    i8_scale: torch.Tensor
+    bias: torch.Tensor | None
+    c: L.Weights = field(default=None, repr=False)
+
+    @classmethod
+    def empty(cls, n: int, k: int, device, bias: torch.Tensor | None = None):
+        d = dict(device=device)
+        pw = cls(n, k,
+                 torch.empty((n, k // 2), dtype=torch.uint8, **d),
+                 torch.zeros(sf_bytes(n, k), dtype=torch.uint8, **d),
+                 torch.zeros(1, dtype=torch.float32, **d),
+                 torch.empty((n, k), dtype=torch.int8, **d),
+                 torch.empty(n, dtype=torch.float32, **d),
+                 None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous())
+        pw.c = L.Weights(n, k, pw.fp4_codes.data_ptr(), pw.fp4_sf.data_ptr(), pw.fp4_g.data_ptr(),
+                         pw.i8_codes.data_ptr(), pw.i8_scale.data_ptr(),
+                         None if pw.bias is None else pw.bias.data_ptr())
+        return pw
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in
+                   (self.fp4_codes, self.fp4_sf, self.fp4_g, self.i8_codes, self.i8_scale))
+
+
+def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None) -> PackedWeights:
+    """Offline pack of nn.Linear weights W [n, k] (bf16, CUDA) in both formats (R7)."""
+    _check_dev(W, "W", torch.bfloat16)
+    W = W.contiguous()
+    n, k = W.shape
+    pw = PackedWeights.empty(n, k, W.device, bias)
+    L.check("dmpq_pack_weights", L.lib().dmpq_pack_weights(_ptr(W), n, k, ctypes.byref(pw.c), _stream(W.device)))
+    return pw
+
+
+# --------------------------------------------------------------------------- activations
+
+@dataclass
+class QuantAct:
+    fmt: int
+    m: int
+    k: int
+    codes: torch.Tensor
+    sf: torch.Tensor | None = None
+    g: torch.Tensor | None = None
+    row_scale: torch.Tensor | None = None
+    c: L.Act = field(default=None, repr=False)
+
+    @classmethod
+    def empty(cls, fmt: int, m: int, k: int, device, g: torch.Tensor | None = None):
+        d = dict(device=device)
+        if fmt == FMT_NVFP4:
+            if g is None:
+                raise ValueError("an NVFP4 activation needs its global scale tensor g (R3)")
+            a = cls(fmt, m, k, torch.empty((m, k // 2), dtype=torch.uint8, **d),
+                    sf=torch.empty(sf_bytes(m, k), dtype=torch.uint8, **d), g=g)
+            a.c = L.Act(fmt, m, k, a.codes.data_ptr(), a.sf.data_ptr(), g.data_ptr(), None)
+        else:
+            a = cls(fmt, m, k, torch.empty((m, k), dtype=torch.int8, **d),
+                    row_scale=torch.empty(m, dtype=torch.float32, **d))
+            a.c = L.Act(fmt, m, k, a.codes.data_ptr(), None, None, a.row_scale.data_ptr())
+        return a
+
+
+def dmpq_quantize_act(X: torch.Tensor, out_i8: QuantAct | None = None, out_fp4: QuantAct | None = None,
+                      amax_out: torch.Tensor | None = None, layernorm: bool = False, ln_eps: float = 1e-6,
+                      h_out: torch.Tensor | None = None):
+    """Quantize X [m, k] (bf16, CUDA, row stride X.stride(0)) into the given outputs (Eq. 2 / P:115)."""
+    _check_dev(X, "X", torch.bfloat16)
+    if X.stride(1) != 1:
+        raise ValueError("X rows must be contiguous")
+    m, k = X.shape
+    opts = None
+    flags = (L.QF_LAYERNORM if layernorm else 0) | (L.QF_WRITE_H if h_out is not None else 0)
+    if flags:
+        opts = L.QuantOpts(flags, ln_eps, None if h_out is None else h_out.data_ptr(),
+                           0 if h_out is None else h_out.stride(0))
+    L.check("dmpq_quantize_act", L.lib().dmpq_quantize_act(
+        _ptr(X), m, k, X.stride(0), None if opts is None else ctypes.byref(opts),
+        None if out_i8 is None else ctypes.byref(out_i8.c), None if out_fp4 is None else ctypes.byref(out_fp4.c),
+        _ptr(amax_out), _stream(X.device)))
+    return out_i8, out_fp4
+
+
+def dmpq_global_scale(amax: torch.Tensor, div: float, g_out: torch.Tensor):
+    """g = max(fl(amax/div), FLT_MIN) on the device (R3)."""
+    _check_dev(amax, "amax", torch.float32)
+    L.check("dmpq_global_scale", L.lib().dmpq_global_scale(_ptr(amax), div, _ptr(g_out), amax.numel(),
+                                                           _stream(amax.device)))
+    return g_out
+
+
+# --------------------------------------------------------------------------- GEMM
+
+def dmpq_gemm(A: QuantAct, W: PackedWeights, Y: torch.Tensor | None = None, Y32: torch.Tensor | None = None,
+              acc: torch.Tensor | None = None, bias: bool = True, gelu: bool = False,
+              residual: torch.Tensor | None = None, gate: torch.Tensor | None = None):
+    """Y = epilogue(A @ W^T) on tcgen05 (kind::i8 or kind::mxf4nvf4)."""
+    flags = (L.EP_BIAS if (bias and W.bias is not None) else 0) | (L.EP_GELU_TANH if gelu else 0)
+    ep = None
+    if residual is not None:
+        flags |= L.EP_RESIDUAL
+        ep = L.Epilogue(flags, gate.data_ptr(), residual.data_ptr(), residual.stride(0))
+    elif flags:
+        ep = L.Epilogue(flags, None, None, 0)
+    if Y is not None:
+        _check_dev(Y, "Y", torch.bfloat16)
+    L.check("dmpq_gemm", L.lib().dmpq_gemm(
+        ctypes.byref(A.c), ctypes.byref(W.c), None if ep is None else ctypes.byref(ep), _ptr(Y),
+        0 if Y is None else Y.stride(0), _ptr(Y32), _ptr(acc), _stream(A.codes.device)))
+    return Y
+
+
+# --------------------------------------------------------------------------- predictor (host-pure)
+
+def dmpq_derive_tau(alpha: float, beta: float, tau_rel: float, eps_slope: float = 1e-8) -> float:
+    return float(L.lib().dmpq_derive_tau(alpha, beta, tau_rel, eps_slope))
+
+
+def dmpq_predict(stats, tau_gamma, t: int, prev_skipped: bool, metric: int = L.GAMMA_L1):
+    """Eq. 7 routing of one block's layers. Returns (fmts list, gamma or nan, status)."""
+    n = len(tau_gamma)
+    taus = (ctypes.c_double * n)(*[float(x) for x in tau_gamma])
+    fmts = (ctypes.c_uint8 * max(n, 1))()
+    gamma = ctypes.c_double(0.0)
+    st = None if stats is None else (stats if isinstance(stats, L.BlockStats) else L.BlockStats.from_seq(stats))
+    rc = L.lib().dmpq_predict(None if st is None else ctypes.byref(st), taus, n, t, int(bool(prev_skipped)), metric,
+                              fmts, ctypes.byref(gamma))
+    L.check("dmpq_predict", rc, allow=(L.DMPQ_EZERONORM,))
+    return [int(fmts[i]) for i in range(n)], gamma.value, rc
+
+
+# --------------------------------------------------------------------------- TDC
+
+def tdc_step(mode: int, x_in: torch.Tensor, x_out: torch.Tensor, delta: torch.Tensor,
+             stats_out: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """SKIP: x_out = x_in + delta. REFRESH: delta <- x_out - x_in, FP64 stats (Eqs. 3/8/9)."""
+    m, h = x_in.shape
+    L.check("tdc_step", L.lib().tdc_step(mode, _ptr(x_in), _ptr(x_out), _ptr(delta), m, h, _ptr(stats_out),
+                                         _ptr(workspace), _stream(x_in.device)))
+
+
+def tdc_new_state() -> L.TdcState:
+    st = L.TdcState()
+    L.lib().tdc_init(ctypes.byref(st))
+    return st
+
+
+def tdc_decide(st: L.TdcState, cfg: L.TdcConfig, t: int) -> int:
+    return int(L.lib().tdc_decide(ctypes.byref(st), ctypes.byref(cfg), t))
+
+
+def tdc_update(st: L.TdcState, cfg: L.TdcConfig, t: int, decision: int, stats=None) -> None:
+    g = None if stats is None else (stats if isinstance(stats, L.BlockStats) else L.BlockStats.from_seq(stats))
+    L.lib().tdc_update(ctypes.byref(st), ctypes.byref(cfg), t, decision, None if g is None else ctypes.byref(g))

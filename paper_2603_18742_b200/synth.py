@@ -1,0 +1,71 @@
+"""Seeded synthetic inputs shaped like the paper's workloads.
+
+Shared by the tests, bench.py and the oracle-side checks. Holds NO arithmetic of
+the method (no quantization, no statistics): only random tensors. All tensors
+are generated on the CPU with torch.Generator so both sides see identical bytes.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+
+def _gen(seed: int) -> torch.Generator:
+    g = torch.Generator(device="cpu")
+    g.manual_seed(int(seed))
+    return g
+
+
+def dit_activation(m: int, k: int, seed: int, outlier_frac: float = 0.005, tail_frac: float = 0.01) -> torch.Tensor:
+    """Video-DiT-like linear-layer input (bf16 [m, k]): N(0,1) base, a per-token
+    LogNormal(0, 0.5) magnitude (so per-token INT8 scales vary), 0.5% outlier
+    channels scaled by U(10, 50) (DiT channel outliers) and
+    Student-t(4) tails on 1% of entries."""
+    g = _gen(seed)
+    x = torch.randn(m, k, generator=g)
+    x *= torch.exp(0.5 * torch.randn(m, 1, generator=g))
+    n_out = max(1, int(round(outlier_frac * k)))
+    ch = torch.randperm(k, generator=g)[:n_out]
+    x[:, ch] *= 10 + 40 * torch.rand(n_out, generator=g)
+    if tail_frac > 0:
+        mask = torch.rand(m, k, generator=g) < tail_frac
+        # Student-t(4): normal / sqrt(chi2_4 / 4)
+        z = torch.randn(m, k, generator=g)
+        chi = (torch.randn(m, k, 4, generator=g) ** 2).sum(-1)
+        x = torch.where(mask, z / torch.sqrt(chi / 4), x)
+    return x.to(torch.bfloat16)
+
+
+def ffn2_activation(m: int, k: int, seed: int) -> torch.Tensor:
+    """FFN2 input: GELU-tanh of an FFN1-like tensor (skewed, mostly >= -0.17)."""
+    x = dit_activation(m, k, seed).float()
+    return torch.nn.functional.gelu(x, approximate="tanh").to(torch.bfloat16)
+
+
+def linear_weight(n: int, k: int, seed: int):
+    """nn.Linear-like weights W ~ N(0, 1/k) (bf16 [n, k]) and bias ~ N(0, 0.02) (fp32 [n])."""
+    g = _gen(seed)
+    w = (torch.randn(n, k, generator=g) / math.sqrt(k)).to(torch.bfloat16)
+    b = 0.02 * torch.randn(n, generator=g)
+    return w, b
+
+
+def adversarial_rows(k: int) -> torch.Tensor:
+    """Edge-case rows for the quantizers: zero rows, +-0, constant rows, tiny and
+    huge magnitudes, blocks whose E4M3 scale is subnormal, a reciprocal near-tie."""
+    rows = []
+    rows.append(torch.zeros(k))
+    r = torch.zeros(k); r[1::2] = -0.0; rows.append(r)
+    rows.append(torch.full((k,), 3.0))
+    rows.append(torch.full((k,), -1e-30))
+    r = torch.full((k,), 1e30); r[::3] = -2e29; rows.append(r)
+    r = torch.randn(k, generator=_gen(7)) * 1e-3; r[0] = 300.0; rows.append(r)   # subnormal-scale blocks
+    r = torch.zeros(k); r[0::16] = 0.17578125; r[1::16] = 0.03662109375; rows.append(r)  # R4 tie vector
+    r = torch.arange(k, dtype=torch.float32) - k / 2; rows.append(r)
+    return torch.stack(rows).to(torch.bfloat16)
+
+
+def bits(t: torch.Tensor):
+    """bf16 tensor -> numpy uint16 bit patterns (for the oracle)."""
+    return t.contiguous().view(torch.int16).cpu().numpy().view("uint16")

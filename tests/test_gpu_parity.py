@@ -1,0 +1,197 @@
+"""GPU parity of every hot-path kernel against the CPU oracle, through the C ABI.
+
+Bars (north_star): codes, scales, INT8 int32 accumulators, INT8
+GEMM fp32 outputs and TDC deltas bit-exact; NVFP4 GEMM fp32 outputs within
+relative L2 1e-5 of the oracle's fp64 accumulation over identical codes; FP64
+statistics within 1e-9 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_18742_b200 import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_18742_b200 import build, dmpq
+    build.build()
+    return dmpq
+
+
+def _u16(t):
+    return synth.bits(t)
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+QUANT_SHAPES = [(1, 64), (7, 128), (37, 512), (300, 1920), (129, 3072), (3, 7680), (130, 12288)]
+
+
+@pytest.mark.parametrize("m,k", QUANT_SHAPES)
+def test_quantize_nvfp4_bit_exact(D, orc, m, k):
+    x = synth.dit_activation(m, k, seed=m * 7 + k)
+    xd = x.cuda()
+    amax_ref = orc.amax_bf16(_u16(x))
+    g = torch.tensor([orc.global_scale(amax_ref, 1344.0)], device="cuda")
+    a = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+    a.sf.fill_(0xAB)  # poison: padding rows must be zeroed by the kernel
+    amax = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(xd, out_fp4=a, amax_out=amax)
+    torch.cuda.synchronize()
+    codes_ref, sf_ref = orc.nvfp4_quantize(_u16(x), float(g.item()))
+    assert amax.item() == amax_ref
+    assert np.array_equal(a.codes.cpu().numpy(), codes_ref)
+    sf_dev = a.sf.cpu().numpy()
+    assert np.array_equal(orc.sf_unswizzle(sf_dev, m, k), sf_ref)
+    assert np.array_equal(sf_dev, orc.sf_swizzle(sf_ref, m, k)), "padding scales must be zero"
+
+
+@pytest.mark.parametrize("m,k", QUANT_SHAPES)
+def test_quantize_int8_bit_exact(D, orc, m, k):
+    x = synth.ffn2_activation(m, k, seed=m + k)
+    a = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a)
+    torch.cuda.synchronize()
+    codes_ref, s_ref = orc.int8_quantize(_u16(x))
+    assert np.array_equal(a.codes.cpu().numpy(), codes_ref)
+    assert np.array_equal(a.row_scale.cpu().numpy(), s_ref)
+
+
+@pytest.mark.parametrize("k", [64, 128, 1920])
+def test_quantize_adversarial_rows(D, orc, k):
+    """Zero / signed-zero / constant / tiny / huge rows, E4M3-subnormal block scales,
+    saturating blocks (g far below amax/1344) and the R4 reciprocal tie vector."""
+    x = synth.adversarial_rows(k)
+    m = x.shape[0]
+    for g_val in (1.0, orc.global_scale(orc.amax_bf16(_u16(x)), 1344.0), 1e-3):
+        g = torch.tensor([g_val], dtype=torch.float32, device="cuda")
+        a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+        a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+        D.dmpq_quantize_act(x.cuda(), out_i8=a8, out_fp4=a4)
+        torch.cuda.synchronize()
+        c_ref, s_ref = orc.nvfp4_quantize(_u16(x), float(g.item()))
+        assert np.array_equal(a4.codes.cpu().numpy(), c_ref)
+        assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s_ref)
+        i_ref, is_ref = orc.int8_quantize(_u16(x))
+        assert np.array_equal(a8.codes.cpu().numpy(), i_ref)
+        assert np.array_equal(a8.row_scale.cpu().numpy(), is_ref)
+
+
+def test_device_cvt_matches_oracle_sweep(D, orc):
+    """The device E2M1/E4M3 conversions (via the quantizer with g = 1 and a unit
+    block scale) agree with the oracle's exhaustive nearest search on a dense
+    sweep of bf16 values around every E2M1 midpoint."""
+    k = 1024
+    vals = []
+    mags = [0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0]
+    for i in range(7):
+        mid = (mags[i] + mags[i + 1]) / 2
+        c = torch.tensor([mid], dtype=torch.bfloat16).view(torch.int16).item()
+        for d in range(-40, 41):
+            vals.append(c + d)
+    v = torch.tensor(vals, dtype=torch.int16).view(torch.bfloat16).float()
+    v = torch.cat([v, -v])
+    n = (v.numel() + 14) // 15
+    rows = torch.zeros(n * 15)
+    rows[: v.numel()] = v
+    rows = rows.view(n, 15)
+    blocks = torch.cat([torch.full((n, 1), 6.0), rows], dim=1)  # block max 6 -> scale exactly 1 (E4M3 0x38)
+    x = blocks.reshape(-1)
+    x = torch.cat([x, torch.zeros((-x.numel()) % k)]).view(-1, k).to(torch.bfloat16)
+    m = x.shape[0]
+    g = torch.ones(1, device="cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+    D.dmpq_quantize_act(x.cuda(), out_fp4=a4)
+    torch.cuda.synchronize()
+    c_ref, s_ref = orc.nvfp4_quantize(_u16(x), 1.0)
+    assert np.array_equal(a4.codes.cpu().numpy(), c_ref)
+
+
+@pytest.mark.parametrize("n,k", [(32, 64), (256, 128), (512, 1920), (1920, 256)])
+def test_pack_weights_bit_exact(D, orc, n, k):
+    w, b = synth.linear_weight(n, k, seed=n + k)
+    pw = D.dmpq_pack_weights(w.cuda(), b)
+    torch.cuda.synchronize()
+    ref = orc.pack_weights(_u16(w))
+    assert pw.fp4_g.item() == ref["fp4_g"]
+    assert np.array_equal(pw.fp4_codes.cpu().numpy(), ref["fp4_codes"])
+    assert np.array_equal(orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k), ref["fp4_sf"])
+    assert np.array_equal(pw.i8_codes.cpu().numpy(), ref["i8_codes"])
+    assert np.array_equal(pw.i8_scale.cpu().numpy(), ref["i8_scale"])
+
+
+GEMM_SHAPES = [(1, 32, 64), (100, 128, 128), (129, 256, 512), (300, 512, 1920), (257, 1920, 256), (64, 96, 3072)]
+
+
+@pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
+def test_gemm_int8_bit_exact(D, orc, m, n, k):
+    x = synth.dit_activation(m, k, seed=3 * m + k)
+    w, b = synth.linear_weight(n, k, seed=n * 3 + k)
+    pw = D.dmpq_pack_weights(w.cuda(), b)
+    a = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a)
+    y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    y32 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    acc = torch.empty(m, n, dtype=torch.int32, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y, Y32=y32, acc=acc)
+    torch.cuda.synchronize()
+    acc_ref, y_ref = orc.gemm_int8(a.codes.cpu().numpy(), a.row_scale.cpu().numpy(), pw.i8_codes.cpu().numpy(),
+                                   pw.i8_scale.cpu().numpy(), b.numpy())
+    assert np.array_equal(acc.cpu().numpy(), acc_ref)
+    assert np.array_equal(y32.cpu().numpy(), y_ref)
+    assert torch.equal(y.cpu(), torch.from_numpy(y_ref).to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
+def test_gemm_nvfp4_rel_l2(D, orc, m, n, k):
+    x = synth.dit_activation(m, k, seed=5 * m + k)
+    w, b = synth.linear_weight(n, k, seed=n * 5 + k)
+    pw = D.dmpq_pack_weights(w.cuda(), b)
+    g = torch.tensor([orc.global_scale(orc.amax_bf16(_u16(x)), 2688.0)], device="cuda")
+    a = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+    D.dmpq_quantize_act(x.cuda(), out_fp4=a)
+    y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    y32 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y, Y32=y32)
+    torch.cuda.synchronize()
+    ref = orc.gemm_nvfp4(a.codes.cpu().numpy(), orc.sf_unswizzle(a.sf.cpu().numpy(), m, k), g.item(),
+                         pw.fp4_codes.cpu().numpy(), orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k),
+                         pw.fp4_g.item(), b.numpy())
+    err = rel_l2(y32.cpu().numpy(), ref)
+    assert err <= 1e-5, err
+    assert torch.equal(y.cpu(), y32.cpu().to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("m,h", [(1, 8), (256, 128), (1000, 1920), (777, 3072)])
+def test_tdc_refresh_and_skip(D, orc, m, h):
+    xi = synth.dit_activation(m, h, seed=m + 1, outlier_frac=0, tail_frac=0)
+    xo = (xi.float() + 0.05 * synth.dit_activation(m, h, seed=m + 2, outlier_frac=0, tail_frac=0).float()).to(torch.bfloat16)
+    dp = (0.05 * synth.dit_activation(m, h, seed=m + 3, outlier_frac=0, tail_frac=0).float()).to(torch.bfloat16)
+    delta = dp.cuda().clone()
+    stats = torch.zeros(7, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(D.tdc_workspace_bytes(m, h), dtype=torch.uint8, device="cuda")
+    D.tdc_step(1, xi.cuda(), xo.cuda(), delta, stats, ws)
+    torch.cuda.synchronize()
+    dn_ref, st_ref = orc.block_stats(_u16(xi), _u16(xo), _u16(dp))
+    assert np.array_equal(synth.bits(delta.cpu()), dn_ref)
+    np.testing.assert_allclose(stats.cpu().numpy(), st_ref, rtol=1e-9, atol=0)
+    # determinism: a second refresh over identical inputs gives identical bits
+    delta2 = dp.cuda().clone()
+    stats2 = torch.zeros(7, dtype=torch.float64, device="cuda")
+    D.tdc_step(1, xi.cuda(), xo.cuda(), delta2, stats2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(stats.cpu(), stats2.cpu())
+    # SKIP, in place
+    x = xi.cuda().clone()
+    D.tdc_step(0, x, x, delta)
+    torch.cuda.synchronize()
+    assert np.array_equal(synth.bits(x.cpu()), orc.tdc_skip(_u16(xi), dn_ref))
