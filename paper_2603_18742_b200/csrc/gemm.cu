@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -381,6 +382,11 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfb_row_tiles = (n + 127) / 128;
         p.num_m_tiles = (m + BM - 1) / BM;
         p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
+        const char* v = getenv("DMPQ_FP4_VARIANT");
+        if (v && v[0] == '1') {
+            p.num_n_tiles = (n + 127) / 128;
+            return launch_gemm<true, 128, 6, 2>(p, A->codes, W->fp4_codes, st);
+        }
         constexpr int BN = 256;
         p.num_n_tiles = (n + BN - 1) / BN;
         return launch_gemm<true, BN, 4, 1>(p, A->codes, W->fp4_codes, st);

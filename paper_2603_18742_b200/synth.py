@@ -69,3 +69,39 @@ def adversarial_rows(k: int) -> torch.Tensor:
 def bits(t: torch.Tensor):
     """bf16 tensor -> numpy uint16 bit patterns (for the oracle)."""
     return t.contiguous().view(torch.int16).cpu().numpy().view("uint16")
+
+
+def linear_weight_device(n: int, k: int, seed: int, device):
+    """Device-side variant of linear_weight (same distribution; different stream of
+    random numbers) for the large bench models, where CPU generation is too slow."""
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    w = (torch.randn(n, k, generator=g, device=device) / math.sqrt(k)).to(torch.bfloat16)
+    b = 0.02 * torch.randn(n, generator=g, device=device)
+    return w, b
+
+
+def trajectory_basis(m: int, h: int, seed: int, device=None):
+    """Two bf16-valued basis tensors A, B [m, h] for the synthetic PF-ODE-like
+    block-0 input X_t = cos(theta_t) A + sin(theta_t) B (a smooth, locally
+    linear trajectory), with per-token magnitudes and a few outlier channels."""
+    if device is None or str(device) == "cpu":
+        a = dit_activation(m, h, seed, tail_frac=0.0).float()
+        b = dit_activation(m, h, seed + 1, tail_frac=0.0).float()
+        return a, b
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    out = []
+    for _ in range(2):
+        x = torch.randn(m, h, generator=g, device=device)
+        x *= torch.exp(0.5 * torch.randn(m, 1, generator=g, device=device))
+        ch = torch.randperm(h, generator=g, device=device)[: max(1, h // 200)]
+        x[:, ch] *= 10 + 40 * torch.rand(ch.numel(), generator=g, device=device)
+        out.append(x)
+    return out[0], out[1]
+
+
+def trajectory_input(A: torch.Tensor, B: torch.Tensor, t: int, T: int, kappa: float = 0.6) -> torch.Tensor:
+    """X_t = cos(theta_t) A + sin(theta_t) B with theta_t = kappa * t / T (bf16)."""
+    th = kappa * t / T
+    return (math.cos(th) * A + math.sin(th) * B).to(torch.bfloat16)

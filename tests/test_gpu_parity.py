@@ -183,7 +183,11 @@ def test_tdc_refresh_and_skip(D, orc, m, h):
     torch.cuda.synchronize()
     dn_ref, st_ref = orc.block_stats(_u16(xi), _u16(xo), _u16(dp))
     assert np.array_equal(synth.bits(delta.cpu()), dn_ref)
-    np.testing.assert_allclose(stats.cpu().numpy(), st_ref, rtol=1e-9, atol=0)
+    # Gamma/L2 sums: FP32 per 8-element vector (<= 7 roundings, 4.2e-7 relative of
+    # the sum of |terms|, all terms non-negative); cosine sums: FP64 per element.
+    st = stats.cpu().numpy()
+    np.testing.assert_allclose(st[:4], st_ref[:4], rtol=4.2e-7, atol=0)
+    np.testing.assert_allclose(st[4:], st_ref[4:], rtol=1e-12, atol=1e-300)
     # determinism: a second refresh over identical inputs gives identical bits
     delta2 = dp.cuda().clone()
     stats2 = torch.zeros(7, dtype=torch.float64, device="cuda")
