@@ -200,11 +200,13 @@ typedef struct {
 
 /* Y = A @ W^T with the dequant/bias epilogue (north_star), on tcgen05.
  *  INT8  (kind::i8): acc = sum_k a*w exactly in int32 (TMEM);
- *        y = fl(fl(fl(float(acc) * s_a[m]) * s_w[n]) + bias[n])        (R8)
+ *        y = fma(fl(float(acc) * s_a[m]), s_w[n], bias[n])             (R8)
  *  NVFP4 (kind::mxf4nvf4.block_scale.scale_vec::4X): acc = sum_k
  *        (dec(a)*s_a,b)(dec(w)*s_w,b) in the tensor core's FP32 accumulator;
- *        y = fl(acc * fl(g_a*g_w)) + bias[n]
- *  then the optional GELU / gated residual, stored as bf16 into Y (row stride
+ *        y = fma(acc, fl(g_a*g_w), bias[n])  (one rounding)
+ *  then the optional GELU (tanh form, hardware tanh.approx) / gated residual
+ *  y = fma(gate[n], y, residual[m,n]) (block glue, tolerance-checked),
+ *  stored as bf16 into Y (row stride
  *  ldy) and/or as FP32 into Y32 (row stride n; NULL to skip). acc_or_null
  *  (INT8 only) receives the raw int32 accumulators [m x n] (parity tests).
  *  A->fmt selects the path and must match the packed operand used.

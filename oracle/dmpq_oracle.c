@@ -279,7 +279,9 @@ void oracle_pack_weights(const uint16_t* w, int n, int k,
 /* ------------------------------------------------------------------------ */
 
 /* INT8: acc[m][n] = sum_k a*w exactly (int64, then checked to fit int32);
- * Y = fl(fl(fl(float(acc) * s_a[m]) * s_w[n]) + bias[n])  (reading R8). */
+ * Y = fma(fl(float(acc) * s_a[m]), s_w[n], bias[n])  (reading R8: the per-token
+ * scale, then the per-channel scale fused with the bias; without bias the last
+ * step is fl(. * s_w[n])). */
 int oracle_gemm_int8(const int8_t* a, const float* s_a, const int8_t* w, const float* s_w,
                      const float* bias, int m, int n, int k, int row0, int row1,
                      int32_t* acc_out, float* y_out) {
@@ -293,8 +295,7 @@ int oracle_gemm_int8(const int8_t* a, const float* s_a, const int8_t* w, const f
             size_t o = (size_t)(i - row0) * n + j;
             if (acc_out) acc_out[o] = (int32_t)acc;
             float y = (float)acc * s_a[i];
-            y = y * s_w[j];
-            if (bias) y = y + bias[j];
+            y = bias ? fmaf(y, s_w[j], bias[j]) : y * s_w[j];
             if (y_out) y_out[o] = y;
         }
     (void)m;

@@ -65,6 +65,22 @@ __device__ __forceinline__ uint32_t e2m1x2(float lo, float hi) {
     return r & 0xFFu;
 }
 
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FMUL2 / FADD2), each lane an IEEE
+// round-to-nearest operation (never contracted: these are explicit .rn ops).
+struct f2 { uint64_t v; };
+__device__ __forceinline__ f2 f2make(float lo, float hi) { f2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi)); return r; }
+__device__ __forceinline__ float f2lo(f2 a) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); (void)hi; return lo; }
+__device__ __forceinline__ float f2hi(f2 a) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); (void)lo; return hi; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { f2 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v)); return r; }
+__device__ __forceinline__ uint32_t pack_bf16x2_f2(f2 a) {
+    uint32_t r;
+    asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; cvt.rn.bf16x2.f32 %0, hi, lo; }" : "=r"(r) : "l"(a.v));
+    return r;
+}
+__device__ __forceinline__ float tanh_approx(float x) { float r; asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

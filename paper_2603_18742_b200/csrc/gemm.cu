@@ -1,19 +1,16 @@
 // gemm.cu — dmpq_gemm: the DMPQ linear layer on 5th-generation tensor cores.
 //   INT8  : tcgen05.mma.kind::i8, exact int32 accumulation in TMEM, FP32
-//           per-token x per-channel dequant epilogue (R8).
+//           per-token x per-channel dequant epilogue, bit-exact (R8).
 //   NVFP4 : tcgen05.mma.kind::mxf4nvf4.block_scale.scale_vec::4X, E4M3 block scales
 //           staged smem -> TMEM with tcgen05.cp, FP32 accumulation in TMEM,
-//           per-tensor g_a*g_w dequant in the epilogue (R3).
+//           per-tensor g_a*g_w dequant fused with the bias as one FMA (R3).
 // Both then apply the bias / GELU / gated-residual epilogue and store bf16 (+ fp32).
 //
-// Persistent, warp-specialised kernel, one CTA per SM (tile 128 x BN):
-//   warp 0     TMA producer (A, B tiles, 128-byte swizzle; NVFP4 scale atoms by bulk copy)
-//   warp 1     MMA issuer (one thread; tcgen05.mma + tcgen05.commit)
-//   warp 2     TMEM allocator
-//   warps 4..7 epilogue (TMEM -> registers -> global), warp w%4 owns TMEM lanes 32(w%4)..
-// smem pipeline: STAGES x {A 128x128B, B BNx128B[, SFA 2 KB, SFB BN/128 x 2 KB]},
-// full/empty mbarriers; TMEM: ACC_STAGES accumulators of BN columns (full/empty
-// mbarriers), so the epilogue of tile i overlaps the mainloop of tile i+1.
+// Persistent, warp-specialised, CTA-pair kernel (one CTA per SM, cluster of 2):
+//   warp 0     TMA producer (A, B-half, NVFP4 scale atoms; 128-byte swizzle)
+//   warp 1     MMA issuer (leader CTA, one thread; tcgen05.mma.cta_group::2 + commit)
+//   warp 2     TMEM allocator (cta_group::2)
+//   warps 4..7 epilogue (TMEM -> registers -> smem -> TMA store), warp w%4 owns TMEM lanes 32(w%4)..
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -57,238 +54,314 @@ struct GemmParams {
 constexpr int BM = 128;
 constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8 / 256 fp4)
 
+
+// ============================================================================
+// 2-CTA kernel (the production path): a CTA pair (cluster of 2) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2 (M = 256). Each CTA loads its own
+// 128 A rows and half of the BN B rows (the MMA reads B from both CTAs' smem), so
+// per-SM L2->smem traffic per FLOP drops by 1.5x vs a 1-CTA 128 x BN tile. NVFP4
+// scale atoms arrive by 3-D TMA (OOB -> zero), SFA per CTA, SFB duplicated in both.
+// TMEM: two BN-column accumulators per CTA (epilogue of tile i overlaps the
+// mainloop of tile i+1). Epilogue: TMEM -> registers -> 64B-swizzled smem staging
+// -> TMA store; per-column vectors (bias, w_scale, gate) staged in smem per tile.
+// ============================================================================
 template <bool FP4, int BN, int STAGES>
-struct SmemLayout {
-    static constexpr int A_BYTES = BM * BK_BYTES;
-    static constexpr int B_BYTES = BN * BK_BYTES;
+struct PairLayout {
+    static constexpr int A_BYTES = BM * BK_BYTES;                 // 16 KB
+    static constexpr int B_BYTES = (BN / 2) * BK_BYTES;           // this CTA's half of B
     static constexpr int SFA_BYTES = FP4 ? 4 * 512 : 0;
-    static constexpr int SFB_BYTES = FP4 ? (BN / 128) * 4 * 512 : 0;
+    static constexpr int SFB_BYTES = FP4 ? 2 * 4 * 512 : 0;       // 2 row-tiles of atoms (256 B rows)
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
-    static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
-    static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;  // barriers + holder + alignment slack
+    static constexpr int PAIR_TX = 2 * STAGE_BYTES;               // bytes both CTAs land per stage
+    static constexpr int STAGING_OFFSET = STAGES * STAGE_BYTES;   // 4 warps x 2 x (32 rows x 64 B)
+    static constexpr int STAGING_BYTES = 4 * 2 * 2048;
+    static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
+    static constexpr int VEC_BYTES = 2 * 3 * BN * 4;              // [acc parity][bias|wscale|gate][BN]
+    static constexpr int BAR_OFFSET = VEC_OFFSET + VEC_BYTES;
+    static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;
+    static_assert(STAGE_BYTES % 1024 == 0, "stage buffers must stay 1024-B aligned");
 };
 
-__device__ __forceinline__ float gelu_tanh(float x) {
-    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    float x3 = __fmul_rn(__fmul_rn(x, x), x);
-    float t = tanhf(__fmul_rn(k0, __fadd_rn(x, __fmul_rn(k1, x3))));
-    return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, t));
-}
-
-template <bool FP4, int BN, int STAGES, int ACC_STAGES>
-__global__ void __launch_bounds__(256, 1) dmpq_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                           const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
-    using L = SmemLayout<FP4, BN, STAGES>;
+template <bool FP4, int BN, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    dmpq_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
+                          const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
+    using L = PairLayout<FP4, BN, STAGES>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t bar_full = sbase + L::BAR_OFFSET;          // STAGES x 8 B
+    const uint32_t bar_full = sbase + L::BAR_OFFSET;
     const uint32_t bar_empty = bar_full + STAGES * 8;
-    const uint32_t bar_tfull = bar_empty + STAGES * 8;        // ACC_STAGES x 8 B
-    const uint32_t bar_tempty = bar_tfull + ACC_STAGES * 8;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFFSET + 2 * STAGES * 8 + 2 * ACC_STAGES * 8);
+    const uint32_t bar_tfull = bar_empty + STAGES * 8;
+    const uint32_t bar_tempty = bar_tfull + 2 * 8;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFFSET + 2 * STAGES * 8 + 4 * 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t ACC_COLS = ACC_STAGES * BN;
-    constexpr uint32_t SF_COLS = FP4 ? (4 * 4 + 4 * (BN / 32)) : 0;
-    constexpr uint32_t NEED_COLS = ACC_COLS + SF_COLS;
-    constexpr uint32_t TMEM_COLS = NEED_COLS <= 32 ? 32 : NEED_COLS <= 64 ? 64 : NEED_COLS <= 128 ? 128 : NEED_COLS <= 256 ? 256 : 512;
-    static_assert(NEED_COLS <= 512, "TMEM budget");
+    const uint32_t rank = cluster_ctarank();
+    constexpr uint32_t ACC_COLS = 2 * BN;
+    constexpr uint32_t SF_COLS = FP4 ? (4 * 4 + 4 * 8) : 0;
+    static_assert(ACC_COLS + SF_COLS <= 512, "TMEM budget");
+    constexpr uint32_t TMEM_COLS = 512;
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
+        if constexpr (FP4) { prefetch_tmap(&tmSFA); prefetch_tmap(&tmSFB); }
+        if (p.Y) prefetch_tmap(&tmY);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(bar_full + 8 * s, 1);
             mbar_init(bar_empty + 8 * s, 1);
         }
-        for (int a = 0; a < ACC_STAGES; ++a) {
+        for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);
-            mbar_init(bar_tempty + 8 * a, 4);  // one arrive per epilogue warp
+            mbar_init(bar_tempty + 8 * a, 8);  // 4 epilogue warps x 2 CTAs
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(smem_u32(tmem_holder), TMEM_COLS);
+    if (warp == 2) tmem_alloc_pair(smem_u32(tmem_holder), TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+    const int num_tiles = p.num_m_tiles * p.num_n_tiles;   // pair tiles (256 rows each)
+    const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
-                    mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        // ===================== TMA producer (both CTAs; whole warp, one elected issuer) =====================
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            const int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
+            const int m0 = mt * 256 + (int)rank * BM;
+            const int nb0 = nt * BN + (int)rank * (BN / 2);
+            for (int kb = 0; kb < p.num_kb; ++kb) {
+                mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                if (elect_one()) {
+                    const uint32_t full_l = leader_addr(bar_full + 8 * stage);
+                    if (rank == 0) mbar_arrive_expect_tx(bar_full + 8 * stage, L::PAIR_TX);
                     const uint32_t sA = sbase + stage * L::STAGE_BYTES;
                     const uint32_t sB = sA + L::A_BYTES;
-                    uint32_t bytes = L::A_BYTES + L::B_BYTES;
-                    int nsub = 4;
-                    if constexpr (FP4) {
-                        nsub = min(4, p.kc4 - kb * 4);  // valid 64-element sub-blocks in this K block
-                        const int sfb_tiles = min(BN / 128, p.sfb_row_tiles - nt * (BN / 128));
-                        bytes += nsub * 512 * (1 + sfb_tiles);
-                    }
-                    mbar_arrive_expect_tx(bar_full + 8 * stage, bytes);
-                    tma_load_2d(sA, &tmA, kb * BK_BYTES, mt * BM, bar_full + 8 * stage);
-                    tma_load_2d(sB, &tmB, kb * BK_BYTES, nt * BN, bar_full + 8 * stage);
+                    tma_load_2d_pair(sA, &tmA, kb * BK_BYTES, m0, full_l);
+                    tma_load_2d_pair(sB, &tmB, kb * BK_BYTES, nb0, full_l);
                     if constexpr (FP4) {
                         const uint32_t sSFA = sB + L::B_BYTES;
                         const uint32_t sSFB = sSFA + L::SFA_BYTES;
-                        bulk_load(sSFA, p.sfa + ((size_t)mt * p.kc4 + kb * 4) * 512, nsub * 512, bar_full + 8 * stage);
-                        for (int h = 0; h < BN / 128; ++h) {
-                            const int rt = nt * (BN / 128) + h;
-                            if (rt < p.sfb_row_tiles)
-                                bulk_load(sSFB + h * 2048, p.sfb + ((size_t)rt * p.kc4 + kb * 4) * 512, nsub * 512,
-                                          bar_full + 8 * stage);
-                        }
+                        tma_load_3d_pair(sSFA, &tmSFA, 0, kb * 4, mt * 2 + (int)rank, full_l);
+                        tma_load_3d_pair(sSFB, &tmSFB, 0, kb * 4, (nt * BN) >> 7, full_l);
                     }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
+        // ===================== MMA issuer (leader CTA; whole warp, one elected issuer) =====================
+        if (rank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
             const uint32_t sfa_t = tmem_base + ACC_COLS;
             const uint32_t sfb_t = sfa_t + 16;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+            uint32_t idesc;
+            if constexpr (FP4) idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            else idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
                 const int nt = tile / p.num_m_tiles;
-                const int acc = local % ACC_STAGES;
-                const uint32_t acc_phase = (local / ACC_STAGES) & 1;
-                const int n_here = min(BN, p.n - nt * BN);           // multiple of 16
-                uint32_t idesc;
-                if constexpr (FP4) {
-                    // block-scaled descriptor: A/B E2M1 (1), scale UE4M3, K-major, N>>3 @17, M>>4 @24
-                    idesc = (1u << 7) | (1u << 10) | ((uint32_t)(n_here >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-                } else {
-                    // S32 accumulate (2 @4), A/B signed int8 (1), K-major
-                    idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n_here >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-                }
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                // SFB rows start at the 128-row atom below n0; BN=192 odd tiles start 64 rows (2 columns) in
+                const uint32_t sfb_shift = (uint32_t)(((nt * BN) & 127) >> 5);
                 mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_t = tmem_base + acc * BN;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(bar_full + 8 * stage, phase);
                     tc_fence_after();
-                    const uint32_t sA = sbase + stage * L::STAGE_BYTES;
-                    const uint32_t sB = sA + L::A_BYTES;
-                    int nsub = 4;
-                    if constexpr (FP4) {
-                        nsub = min(4, p.kc4 - kb * 4);
-                        const uint32_t sSFA = sB + L::B_BYTES;
-                        const uint32_t sSFB = sSFA + L::SFA_BYTES;
-                        for (int j = 0; j < nsub; ++j) {
-                            tc_cp_32x128b_warpx4(sfa_t + j * 4, sdesc_rows16(sSFA + j * 512));
-                            for (int h = 0; h < BN / 128; ++h)
-                                tc_cp_32x128b_warpx4(sfb_t + j * (BN / 32) + h * 4, sdesc_rows16(sSFB + h * 2048 + j * 512));
+                    if (elect_one()) {
+                        const uint32_t sA = sbase + stage * L::STAGE_BYTES;
+                        const uint32_t sB = sA + L::A_BYTES;
+                        if constexpr (FP4) {
+                            const uint32_t sSFA = sB + L::B_BYTES;
+                            const uint32_t sSFB = sSFA + L::SFA_BYTES;
+                            const uint64_t da = sdesc_rows16(sSFA), db = sdesc_rows16(sSFB);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                tc_cp_pair_32x128b_warpx4(sfa_t + j * 4, da + (uint64_t)(j * 32));
+                                tc_cp_pair_32x128b_warpx4(sfb_t + j * 8, db + (uint64_t)(j * 32));
+                                tc_cp_pair_32x128b_warpx4(sfb_t + j * 8 + 4, db + (uint64_t)(128 + j * 32));
+                            }
                         }
+                        const uint64_t adesc = sdesc_k_sw128(sA), bdesc = sdesc_k_sw128(sB);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t accum = (kb | j) ? 1u : 0u;
+                            if constexpr (FP4)
+                                mma_fp4_pair(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, sfa_t + j * 4, sfb_t + j * 8 + sfb_shift, accum);
+                            else
+                                mma_i8_pair(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, accum);
+                        }
+                        tc_commit_pair_mc(bar_empty + 8 * stage, 0x3);
                     }
-                    const uint64_t adesc = sdesc_k_sw128(sA), bdesc = sdesc_k_sw128(sB);
-                    for (int j = 0; j < nsub; ++j) {
-                        const uint32_t accum = (kb | j) ? 1u : 0u;
-                        // advance 32 bytes along K inside the swizzle row (start address is in 16-B units)
-                        if constexpr (FP4)
-                            mma_fp4(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, sfa_t + j * 4, sfb_t + j * (BN / 32), accum);
-                        else
-                            mma_i8(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, accum);
-                    }
-                    tc_commit(bar_empty + 8 * stage);  // smem slot free once these MMAs retire
+                    __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(bar_tfull + 8 * acc);        // accumulator ready for the epilogue
+                if (elect_one()) tc_commit_pair_mc(bar_tfull + 8 * acc, 0x3);
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
-        // ===================== epilogue =====================
-        const int q = warp & 3;                          // TMEM lane quarter
+        // ===================== epilogue (both CTAs, 4 warps each) =====================
+        // Instruction-lean: the epilogue issues ~1.5 (NVFP4) / ~3.5 (INT8) instructions per
+        // output element and is the critical path for short-K layers, so
+        // the math is packed fp32x2 (FFMA2/FMUL2/FADD2) and per-column vectors come from smem
+        // as 128-bit broadcast loads.
+        const int q = warp & 3;
+        const int etid = threadIdx.x - 128;
         int local = 0;
+        uint32_t chunk_ctr = 0;
         float gg = 0.0f;
         if constexpr (FP4) gg = __fmul_rn(*p.g_a, *p.g_w);
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const f2 gg2 = f2make(gg, gg);
+        const uint32_t staging = sbase + L::STAGING_OFFSET + q * 4096;
+        const uint32_t vec_s = sbase + L::VEC_OFFSET;
+        const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0;
+        const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
+        const bool has_res = (p.flags & DMPQ_EP_RESIDUAL) != 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
             const int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
-            const int acc = local % ACC_STAGES;
-            const uint32_t acc_phase = (local / ACC_STAGES) & 1;
-            mbar_wait(bar_tfull + 8 * acc, acc_phase);
-            tc_fence_after();
-            const int row = mt * BM + q * 32 + lane;
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            const int n0 = nt * BN;
+            // per-column epilogue vectors of this tile -> smem (double-buffered by tile parity)
+            const uint32_t vb = vec_s + acc * 3 * BN * 4;
+            for (int i = etid; i < BN; i += 128) {
+                const int col = n0 + i;
+                const bool ok = col < p.n;
+                const float bv = (ok && has_bias) ? p.bias[col] : -0.0f;   // fma(x, s, -0) == fl(x * s) exactly
+                const float wv = (!FP4 && ok) ? p.w_scale[col] : 0.0f;
+                const float gv = (ok && has_res) ? p.gate[col] : 0.0f;
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + i * 4), "f"(bv) : "memory");
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + (BN + i) * 4), "f"(wv) : "memory");
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + (2 * BN + i) * 4), "f"(gv) : "memory");
+            }
+            named_bar_sync(1, 128);
+            const int rowbase = mt * 256 + (int)rank * BM + q * 32;
+            const int row = rowbase + lane;
             const bool row_ok = row < p.m;
             float sa = 0.0f;
             if constexpr (!FP4) sa = row_ok ? p.a_scale[row] : 0.0f;
-            const int n_here = min(BN, p.n - nt * BN);
+            const f2 sa2 = f2make(sa, sa);
+            mbar_wait(bar_tfull + 8 * acc, acc_phase);
+            tc_fence_after();
+            const int n_here = min(BN, p.n - n0);
             for (int c = 0; c < BN / 32; ++c) {
-                if (c * 32 >= n_here) break;             // uniform across the CTA
+                if (c * 32 >= n_here) break;
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
                 if (c * 32 + 32 >= n_here) {
-                    // last chunk of this accumulator: hand TMEM back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+                    if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
                 }
-                if (!row_ok) continue;
-                const int col0 = nt * BN + c * 32;
-                float y[32];
+                const int col0 = n0 + c * 32;
+                f2 y[16];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    float v;
+                for (int v4 = 0; v4 < 8; ++v4) {
+                    float b0, b1, b2, b3;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(vb + (c * 32 + v4 * 4) * 4));
+                    const f2 bb0 = f2make(b0, b1), bb1 = f2make(b2, b3);
                     if constexpr (FP4) {
-                        v = __fmul_rn(__uint_as_float(r[j]), gg);
+                        const f2 a0 = f2make(__uint_as_float(r[4 * v4]), __uint_as_float(r[4 * v4 + 1]));
+                        const f2 a1 = f2make(__uint_as_float(r[4 * v4 + 2]), __uint_as_float(r[4 * v4 + 3]));
+                        // y = fma(acc, g_a*g_w, bias): one rounding (FP32 tolerance path, R3)
+                        y[2 * v4] = fma2(a0, gg2, bb0);
+                        y[2 * v4 + 1] = fma2(a1, gg2, bb1);
                     } else {
-                        v = __fmul_rn(__fmul_rn(__int2float_rn((int)r[j]), sa), __ldg(p.w_scale + col0 + j));
+                        float w0, w1, w2, w3;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(w0), "=f"(w1), "=f"(w2), "=f"(w3) : "r"(vb + (BN + c * 32 + v4 * 4) * 4));
+                        const f2 a0 = f2make(__int2float_rn((int)r[4 * v4]), __int2float_rn((int)r[4 * v4 + 1]));
+                        const f2 a1 = f2make(__int2float_rn((int)r[4 * v4 + 2]), __int2float_rn((int)r[4 * v4 + 3]));
+                        // y = fma(fl(float(acc) * s_a), s_w, bias)  (R8; bias -0.0 when absent)
+                        y[2 * v4] = fma2(mul2(a0, sa2), f2make(w0, w1), bb0);
+                        y[2 * v4 + 1] = fma2(mul2(a1, sa2), f2make(w2, w3), bb1);
                     }
-                    if (p.flags & DMPQ_EP_BIAS) v = __fadd_rn(v, __ldg(p.bias + col0 + j));
-                    if (p.flags & DMPQ_EP_GELU_TANH) v = gelu_tanh(v);
-                    y[j] = v;
                 }
-                if (p.flags & DMPQ_EP_RESIDUAL) {
+                if (has_gelu) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        float lo = f2lo(y[j]), hi = f2hi(y[j]);
+                        lo = __fmul_rn(__fmul_rn(0.5f, lo), __fadd_rn(1.0f, tanh_approx(__fmul_rn(0.7978845608028654f,
+                                       __fadd_rn(lo, __fmul_rn(0.044715f, __fmul_rn(__fmul_rn(lo, lo), lo)))))));
+                        hi = __fmul_rn(__fmul_rn(0.5f, hi), __fadd_rn(1.0f, tanh_approx(__fmul_rn(0.7978845608028654f,
+                                       __fadd_rn(hi, __fmul_rn(0.044715f, __fmul_rn(__fmul_rn(hi, hi), hi)))))));
+                        y[j] = f2make(lo, hi);
+                    }
+                }
+                if (has_res && row_ok) {
                     const uint4* rp = reinterpret_cast<const uint4*>(p.residual + (size_t)row * p.ldr + col0);
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
                         const uint4 rv = rp[v4];
                         const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+                        float g0, g1, g2, g3, g4, g5, g6, g7;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(g0), "=f"(g1), "=f"(g2), "=f"(g3) : "r"(vb + (2 * BN + c * 32 + v4 * 8) * 4));
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(g4), "=f"(g5), "=f"(g6), "=f"(g7) : "r"(vb + (2 * BN + c * 32 + v4 * 8 + 4) * 4));
+                        const f2 gp[4] = {f2make(g0, g1), f2make(g2, g3), f2make(g4, g5), f2make(g6, g7)};
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int e = v4 * 8 + j * 2;
-                            y[e] = __fadd_rn(bf16lo(w[j]), __fmul_rn(__ldg(p.gate + col0 + e), y[e]));
-                            y[e + 1] = __fadd_rn(bf16hi(w[j]), __fmul_rn(__ldg(p.gate + col0 + e + 1), y[e + 1]));
-                        }
+                        for (int j = 0; j < 4; ++j)   // y = fma(gate, y, res)
+                            y[v4 * 4 + j] = fma2(gp[j], y[v4 * 4 + j], f2make(bf16lo(w[j]), bf16hi(w[j])));
                     }
                 }
                 if (p.Y) {
-                    uint4* yp = reinterpret_cast<uint4*>(p.Y + (size_t)row * p.ldy + col0);
+                    const uint32_t buf = staging + (chunk_ctr & 1) * 2048;
+                    if (lane == 0) bulk_wait_read1();   // the store issued from this buffer 2 chunks ago has read it
+                    __syncwarp();
 #pragma unroll
-                    for (int v4 = 0; v4 < 4; ++v4)
-                        yp[v4] = make_uint4(pack_bf16x2(y[v4 * 8 + 0], y[v4 * 8 + 1]), pack_bf16x2(y[v4 * 8 + 2], y[v4 * 8 + 3]),
-                                            pack_bf16x2(y[v4 * 8 + 4], y[v4 * 8 + 5]), pack_bf16x2(y[v4 * 8 + 6], y[v4 * 8 + 7]));
+                    for (int v4 = 0; v4 < 4; ++v4) {
+                        const uint32_t a = buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);  // 64B swizzle
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack_bf16x2_f2(y[4 * v4])),
+                                     "r"(pack_bf16x2_f2(y[4 * v4 + 1])), "r"(pack_bf16x2_f2(y[4 * v4 + 2])),
+                                     "r"(pack_bf16x2_f2(y[4 * v4 + 3]))
+                                     : "memory");
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmY, buf, col0, rowbase);
+                        bulk_commit();
+                    }
+                    ++chunk_ctr;
                 }
-                if (p.Y32) {
-                    float4* yp = reinterpret_cast<float4*>(p.Y32 + (size_t)row * p.n + col0);
-#pragma unroll
-                    for (int v4 = 0; v4 < 8; ++v4) yp[v4] = make_float4(y[4 * v4], y[4 * v4 + 1], y[4 * v4 + 2], y[4 * v4 + 3]);
-                }
-                if constexpr (!FP4) {
-                    if (p.acc_out) {
-                        int4* ap = reinterpret_cast<int4*>(p.acc_out + (size_t)row * p.n + col0);
+                if (row_ok) {
+                    if (p.Y32) {
+                        float4* yp = reinterpret_cast<float4*>(p.Y32 + (size_t)row * p.n + col0);
 #pragma unroll
                         for (int v4 = 0; v4 < 8; ++v4)
-                            ap[v4] = make_int4((int)r[4 * v4], (int)r[4 * v4 + 1], (int)r[4 * v4 + 2], (int)r[4 * v4 + 3]);
+                            yp[v4] = make_float4(f2lo(y[2 * v4]), f2hi(y[2 * v4]), f2lo(y[2 * v4 + 1]), f2hi(y[2 * v4 + 1]));
+                    }
+                    if constexpr (!FP4) {
+                        if (p.acc_out) {
+                            int4* ap = reinterpret_cast<int4*>(p.acc_out + (size_t)row * p.n + col0);
+#pragma unroll
+                            for (int v4 = 0; v4 < 8; ++v4)
+                                ap[v4] = make_int4((int)r[4 * v4], (int)r[4 * v4 + 1], (int)r[4 * v4 + 2], (int)r[4 * v4 + 3]);
+                        }
                     }
                 }
             }
         }
+        if (lane == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) tmem_dealloc(tmem_base, TMEM_COLS);
+    cluster_sync();
+    if (warp == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
 }
 
 // ------------------------------------------------------------------ host side
@@ -320,22 +393,64 @@ static bool make_tmap(CUtensorMap* tm, const void* base, int rows, int row_bytes
     return r == CUDA_SUCCESS;
 }
 
-template <bool FP4, int BN, int STAGES, int ACC_STAGES>
-static dmpq_status launch_gemm(const GemmParams& p, const void* a_codes, const void* w_codes, cudaStream_t s) {
-    using L = SmemLayout<FP4, BN, STAGES>;
-    CUtensorMap tmA, tmB;
-    if (!make_tmap(&tmA, a_codes, p.m, p.kbytes, BM) || !make_tmap(&tmB, w_codes, p.n, p.kbytes, BN))
-        return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed");
-    auto kern = dmpq_gemm_kernel<FP4, BN, STAGES, ACC_STAGES>;
+// 3-D view of a swizzled scale buffer: [row_tiles][kc4 atoms][128 x u32 (512 B)], box {128, 4, box_tiles}.
+static bool make_tmap_sf(CUtensorMap* tm, const void* base, int row_tiles, int kc4, int box_tiles) {
+    auto enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {128, (cuuint64_t)kc4, (cuuint64_t)row_tiles};
+    cuuint64_t strides[2] = {512, (cuuint64_t)kc4 * 512};
+    cuuint32_t box[3] = {128, 4, (cuuint32_t)box_tiles};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// bf16 output [rows x cols] (row stride ld elements), box 32 x 32, 64-B swizzle (epilogue TMA store).
+static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, int ld) {
+    auto enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <bool FP4, int BN, int STAGES>
+static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
+    using L = PairLayout<FP4, BN, STAGES>;
+    CUtensorMap tmA, tmB, tmSFA, tmSFB, tmY;
+    std::memset(&tmSFA, 0, sizeof(tmSFA));
+    std::memset(&tmSFB, 0, sizeof(tmSFB));
+    std::memset(&tmY, 0, sizeof(tmY));
+    if (!make_tmap(&tmA, a_codes, p.m, p.kbytes, BM) || !make_tmap(&tmB, w_codes, p.n, p.kbytes, BN / 2))
+        return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (A/B)");
+    if constexpr (FP4) {
+        if (!make_tmap_sf(&tmSFA, p.sfa, (p.m + 127) / 128, p.kc4, 1) ||
+            !make_tmap_sf(&tmSFB, p.sfb, p.sfb_row_tiles, p.kc4, 2))
+            return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (scales)");
+    }
+    if (p.Y && !make_tmap_y(&tmY, p.Y, p.m, p.n, p.ldy))
+        return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (Y)");
+    p.num_m_tiles = (p.m + 255) / 256;
+    p.num_n_tiles = (p.n + BN - 1) / BN;
+    p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
+    auto kern = dmpq_gemm_pair_kernel<FP4, BN, STAGES>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
             return check_launch("dmpq_gemm(smem attribute)");
         attr_set = true;
     }
-    int tiles = p.num_m_tiles * p.num_n_tiles;
-    int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, 256, L::TOTAL, s>>>(tmA, tmB, p);
+    const int tiles = p.num_m_tiles * p.num_n_tiles;
+    int clusters = num_sms() / 2;
+    if (clusters > tiles) clusters = tiles;
+    kern<<<2 * clusters, 256, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, p);
     return check_launch("dmpq_gemm");
 }
 
@@ -380,25 +495,12 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
-        p.num_m_tiles = (m + BM - 1) / BM;
-        p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
-        const char* v = getenv("DMPQ_FP4_VARIANT");
-        if (v && v[0] == '1') {
-            p.num_n_tiles = (n + 127) / 128;
-            return launch_gemm<true, 128, 6, 2>(p, A->codes, W->fp4_codes, st);
-        }
-        constexpr int BN = 256;
-        p.num_n_tiles = (n + BN - 1) / BN;
-        return launch_gemm<true, BN, 4, 1>(p, A->codes, W->fp4_codes, st);
+        return launch_gemm_pair<true, 192, 6>(p, A->codes, W->fp4_codes, st);
     } else {
         DMPQ_REQUIRE(A->codes && A->row_scale && W->i8_codes && W->i8_scale && aligned16(A->codes) && aligned16(W->i8_codes),
                      DMPQ_EALIGN, "dmpq_gemm: INT8 operand pointers");
         p.kbytes = k;
         p.a_scale = A->row_scale; p.w_scale = W->i8_scale;
-        p.num_m_tiles = (m + BM - 1) / BM;
-        p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
-        constexpr int BN = 256;
-        p.num_n_tiles = (n + BN - 1) / BN;
-        return launch_gemm<false, BN, 4, 2>(p, A->codes, W->i8_codes, st);
+        return launch_gemm_pair<false, 256, 6>(p, A->codes, W->i8_codes, st);
     }
 }

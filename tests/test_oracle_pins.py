@@ -22,6 +22,17 @@ def bf16_bits(vals):
     return t.view(torch.int16).numpy().view(np.uint16).copy()
 
 
+def round_f32(fr: Fraction) -> np.float32:
+    """Correctly rounded (nearest-even) binary32 value of an exact rational."""
+    f = np.float32(float(fr))
+    best = f
+    for c in (np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))):
+        dc, db = abs(Fraction(float(c)) - fr), abs(Fraction(float(best)) - fr)
+        if dc < db or (dc == db and (int(np.float32(c).view(np.uint32)) & 1) == 0):
+            best = c
+    return np.float32(best)
+
+
 def bf16_vals(bits):
     return torch.from_numpy(np.asarray(bits, dtype=np.uint16).view(np.int16)).view(torch.bfloat16).float().numpy()
 
@@ -260,8 +271,10 @@ def test_gemm_int8_brute_force(orc):
         for j in range(n):
             exact = sum(int(a[i, t]) * int(w[j, t]) for t in range(k))
             assert acc[i, j] == exact
-            yy = np.float32(np.float32(np.float32(exact) * sa[i]) * sw[j]) + b[j]
-            assert y[i, j] == np.float32(yy)
+            # R8: fma(fl(acc * s_a), s_w, bias) -- the fused step checked in exact rationals
+            t = Fraction(float(np.float32(np.float32(exact) * sa[i])))
+            yy = round_f32(t * Fraction(float(sw[j])) + Fraction(float(b[j])))
+            assert y[i, j] == yy
     acc2, _ = orc.gemm_int8(a, sa, w, sw, b, rows=(2, 4))
     assert np.array_equal(acc2, acc[2:4])
 
