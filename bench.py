@@ -98,10 +98,6 @@ def dist_setup(args):
     return 0, 1, 0, None
 
 
-def shard_rows(M: int, world: int, rank: int):
-    return (M * rank) // world, (M * (rank + 1)) // world
-
-
 # ------------------------------------------------------------------------------------------ CPU oracle
 def cpu_oracle_sample(H: int, F: int, rows: int, nvfp4_frac: float, seed: int = 7):
     """Time the CPU oracle (oracle/, single-threaded C) on a bounded sample: the
@@ -170,6 +166,7 @@ def run_ours(args):
     from paper_2603_18742_b200 import dmpq as D
     from paper_2603_18742_b200 import synth
     from paper_2603_18742_b200.block import DiTStack
+    from paper_2603_18742_b200.shard import shard_rows
 
     build.build()
     rank, world, local, group = dist_setup(args)

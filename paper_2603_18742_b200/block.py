@@ -32,6 +32,7 @@ import torch
 from . import _lib as L
 from . import dmpq as D
 from . import synth
+from .shard import exchange
 
 LAYERS = ("q", "k", "v", "o", "ffn1", "ffn2")
 SLOT_OF_LAYER = (0, 0, 0, 1, 2, 3)   # activation tensor each layer consumes
@@ -140,6 +141,20 @@ class DiTStack:
         self.timing = False                     # record CUDA events around every GEMM (roofline)
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0}
+        self.capture = None                     # dict -> per-stage clones for the parity tests
+
+    def _cap(self, key, t):
+        if self.capture is not None:
+            self.capture[key] = t.detach().clone()
+
+    def _cap_act(self, key, a):
+        if self.capture is not None and a is not None:
+            d = {"codes": a.codes.clone()}
+            if a.fmt == D.FMT_NVFP4:
+                d.update(sf=a.sf.clone(), g=a.g.clone())
+            else:
+                d.update(row_scale=a.row_scale.clone())
+            self.capture[key] = d
 
     # ------------------------------------------------------------------ one block
     def _compute_block(self, b: int, x_in: torch.Tensor, x_out: torch.Tensor, fmts) -> float:
@@ -149,22 +164,36 @@ class DiTStack:
         need = set(fmts[0:3])
         a0_i8 = ws.act(0, D.FMT_INT8, b) if D.FMT_INT8 in need else None
         a0_f4 = ws.act(0, D.FMT_NVFP4, b) if D.FMT_NVFP4 in need else None
-        D.dmpq_quantize_act(x_in, out_i8=a0_i8, out_fp4=a0_f4, amax_out=amax[0:1], layernorm=True)
+        cap = self.capture is not None
+        h1 = torch.empty(m, H, dtype=torch.bfloat16, device=x_in.device) if cap else None
+        D.dmpq_quantize_act(x_in, out_i8=a0_i8, out_fp4=a0_f4, amax_out=amax[0:1], layernorm=True, h_out=h1)
+        if cap:
+            self._cap("x_in", x_in); self._cap("h1", h1)
+            self._cap_act("a0_i8", a0_i8); self._cap_act("a0_f4", a0_f4)
         for j, out in ((0, ws.qk), (1, ws.qk), (2, ws.v)):
             a = a0_i8 if fmts[j] == D.FMT_INT8 else a0_f4
             self._gemm(a, W.layers[j], Y=out)
+            self._cap(f"y{j}", out)
         # O projection on the attention stand-in a = v, gated residual in the epilogue
         a1 = ws.act(1, fmts[3], b)
         D.dmpq_quantize_act(ws.v, **{("out_i8" if fmts[3] == D.FMT_INT8 else "out_fp4"): a1}, amax_out=amax[1:2])
+        self._cap_act("a1", a1)
         self._gemm(a1, W.layers[3], Y=ws.x_mid, residual=x_in, gate=W.g1)
+        self._cap("x_mid", ws.x_mid)
         # FFN
         a2 = ws.act(2, fmts[4], b)
+        h2 = torch.empty(m, H, dtype=torch.bfloat16, device=x_in.device) if cap else None
         D.dmpq_quantize_act(ws.x_mid, **{("out_i8" if fmts[4] == D.FMT_INT8 else "out_fp4"): a2},
-                            amax_out=amax[2:3], layernorm=True)
+                            amax_out=amax[2:3], layernorm=True, h_out=h2)
+        if cap:
+            self._cap("h2", h2); self._cap_act("a2", a2)
         self._gemm(a2, W.layers[4], Y=ws.f, gelu=True)
+        self._cap("f", ws.f)
         a3 = ws.act(3, fmts[5], b)
         D.dmpq_quantize_act(ws.f, **{("out_i8" if fmts[5] == D.FMT_INT8 else "out_fp4"): a3}, amax_out=amax[3:4])
+        self._cap_act("a3", a3)
         self._gemm(a3, W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
+        self._cap("x_out", x_out)
         self.launches += 4 + 6
         return 2.0 * m * (4 * H * H + 2 * H * F)
 
@@ -226,15 +255,10 @@ class DiTStack:
         """Per-step exchange + host decisions: combine the statistics of all ranks
         (slot-packed SUM all-reduce = exact all-gather; MAX all-reduce for amax), copy
         them to the host once, update TDC (Eq. 10) and the NVFP4 global scales (R3)."""
-        if self.group is not None and self.world > 1:
-            torch.distributed.all_reduce(self.stats_slots, op=torch.distributed.ReduceOp.SUM, group=self.group)
-            torch.distributed.all_reduce(self.amax, op=torch.distributed.ReduceOp.MAX, group=self.group)
+        # one exchange per step; the D2H copy inside synchronises the stream
+        stats = exchange(self.stats_slots, self.amax, self.group, self.world)
         D.dmpq_global_scale(self.amax.view(-1), 1344.0, self.g_table.view(-1))
         self.launches += 1
-        slots = self.stats_slots.cpu().numpy()          # synchronises the stream
-        stats = np.zeros((self.nb, L.STATS_LEN))
-        for r in range(self.world):                     # rank-ordered combine: identical on every rank
-            stats += slots[r]
         rec = self.records[-1]
         for b in range(self.nb):
             d = rec.decisions[b]

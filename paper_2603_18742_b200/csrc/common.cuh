@@ -69,8 +69,8 @@ __device__ __forceinline__ uint32_t e2m1x2(float lo, float hi) {
 // round-to-nearest operation (never contracted: these are explicit .rn ops).
 struct f2 { uint64_t v; };
 __device__ __forceinline__ f2 f2make(float lo, float hi) { f2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi)); return r; }
-__device__ __forceinline__ float f2lo(f2 a) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); (void)hi; return lo; }
-__device__ __forceinline__ float f2hi(f2 a) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v)); (void)lo; return hi; }
+__device__ __forceinline__ float f2lo(f2 a) { return __uint_as_float((uint32_t)a.v); }
+__device__ __forceinline__ float f2hi(f2 a) { return __uint_as_float((uint32_t)(a.v >> 32)); }
 __device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
 __device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v)); return r; }
 __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { f2 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v)); return r; }

@@ -101,7 +101,7 @@ def trajectory_basis(m: int, h: int, seed: int, device=None):
     return out[0], out[1]
 
 
-def trajectory_input(A: torch.Tensor, B: torch.Tensor, t: int, T: int, kappa: float = 0.6) -> torch.Tensor:
+def trajectory_input(A: torch.Tensor, B: torch.Tensor, t: int, T: int, kappa: float = 0.05) -> torch.Tensor:
     """X_t = cos(theta_t) A + sin(theta_t) B with theta_t = kappa * t / T (bf16)."""
     th = kappa * t / T
     return (math.cos(th) * A + math.sin(th) * B).to(torch.bfloat16)

@@ -1,0 +1,211 @@
+"""Block-step parity (BASELINE configs[0]: one DiT block, hidden 128, FFN 512,
+256 tokens, 4 timesteps) through the C ABI, teacher-forced stage by stage
+against the oracle:
+
+  - every quantization stage: codes and scales bit-exact given the GPU's input;
+  - INT8 GEMM stages: bit-exact given the GPU's codes (epilogue incl. residual);
+  - NVFP4 GEMM stages and the glue (LN, GELU): tolerance;
+  - TDC refresh: delta bit-exact, statistics within their bounds;
+  - per-step routing and TDC decisions equal to the oracle's, taken from the GPU's
+    statistics, except values within 1e-6 relative of a threshold.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_18742_b200 import synth  # noqa: E402
+
+
+def bits(t):
+    return synth.bits(t.detach().cpu())
+
+
+def f32(t):
+    return t.detach().cpu().float().numpy().astype(np.float64)
+
+
+def close_bf16(gpu_bf16, ref64, rel=2.0 ** -7):
+    g = f32(gpu_bf16)
+    err = np.abs(g - ref64)
+    scale = np.maximum(np.abs(ref64), 1e-3 * np.abs(ref64).max())
+    assert np.all(err <= rel * scale + 1e-30), float((err / scale).max())
+    assert np.linalg.norm(g - ref64) <= 4e-3 * np.linalg.norm(ref64)
+
+
+@pytest.fixture(scope="module")
+def run():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_18742_b200 import build
+    from paper_2603_18742_b200.block import DiTStack
+    build.build()
+    dev = torch.device("cuda")
+    M, H, F, T = 256, 128, 512, 6
+    # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
+    stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008])
+    A, B = synth.trajectory_basis(M, H, seed=77)
+    steps = []
+    for t in range(T):
+        x = synth.trajectory_input(A, B, t, 50).to(dev)
+        cap = {}
+        stack.capture = cap
+        d0 = stack.delta[0].clone()
+        g_before = stack.g_table.clone()
+        stack.step(x, t)
+        stats = stack.end_step(t)
+        rec = stack.records[-1]
+        steps.append(dict(t=t, cap=cap, x=x.cpu(), delta_prev=d0.cpu(), delta_new=stack.delta[0].clone().cpu(),
+                          stats=stats[0].copy(), fmts=rec.fmts[0], decision=rec.decisions[0],
+                          g=g_before.cpu(), out=stack.x_buf[0].clone().cpu()))
+    return stack, steps
+
+
+def _ln64(x):
+    x = x.astype(np.float64)
+    mu = x.mean(axis=1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=1, keepdims=True)
+    return (x - mu) / np.sqrt(var + 1e-6)
+
+
+def _check_quant(orc, src_bf16, act, fmt, k):
+    from paper_2603_18742_b200 import dmpq as D
+    m = src_bf16.shape[0]
+    if fmt == D.FMT_NVFP4:
+        g = float(act["g"].item())
+        c, s = orc.nvfp4_quantize(bits(src_bf16), g)
+        assert np.array_equal(act["codes"].cpu().numpy(), c)
+        assert np.array_equal(orc.sf_unswizzle(act["sf"].cpu().numpy(), m, k), s)
+        return c, s, g
+    c, s = orc.int8_quantize(bits(src_bf16))
+    assert np.array_equal(act["codes"].cpu().numpy(), c)
+    assert np.array_equal(act["row_scale"].cpu().numpy(), s)
+    return c, s, None
+
+
+def _gemm_ref(orc, fmt, q, pw, n, k):
+    """fp64/fp32 oracle output of one layer from the GPU's codes (teacher forcing)."""
+    from paper_2603_18742_b200 import dmpq as D
+    bias = pw.bias.cpu().numpy()
+    if fmt == D.FMT_NVFP4:
+        c, s, g = q
+        return orc.gemm_nvfp4(c, s, g, pw.fp4_codes.cpu().numpy(), orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k),
+                              pw.fp4_g.item(), bias), False
+    c, s, _ = q
+    _, y = orc.gemm_int8(c, s, pw.i8_codes.cpu().numpy(), pw.i8_scale.cpu().numpy(), bias)
+    return y.astype(np.float64), True
+
+
+def test_stages_teacher_forced(run, orc):
+    from paper_2603_18742_b200 import dmpq as D
+    stack, steps = run
+    W = stack.blocks[0]
+    H, F = stack.H, stack.F
+    n_checked = 0
+    for st in steps:
+        if st["fmts"] is None:
+            continue
+        cap, fm = st["cap"], st["fmts"]
+        n_checked += 1
+        # LN glue (tolerance), then quantizers bit-exact on the GPU's h
+        close_bf16(cap["h1"], _ln64(f32(cap["x_in"])))
+        qs = {}
+        for f_ in set(fm[0:3]):
+            qs[f_] = _check_quant(orc, cap["h1"], cap["a0_i8" if f_ == D.FMT_INT8 else "a0_f4"], f_, H)
+        for j in range(3):
+            ref, exact = _gemm_ref(orc, fm[j], qs[fm[j]], W.layers[j], H, H)
+            if exact:
+                assert torch.equal(cap[f"y{j}"].cpu(), torch.from_numpy(ref.astype(np.float32)).to(torch.bfloat16))
+            else:
+                close_bf16(cap[f"y{j}"], ref)
+        # O projection on a = v with the gated residual
+        q1 = _check_quant(orc, cap["y2"], cap["a1"], fm[3], H)
+        yo, exact = _gemm_ref(orc, fm[3], q1, W.layers[3], H, H)
+        gate = W.g1.cpu().numpy()
+        xin = f32(cap["x_in"])
+        if exact:   # fma(gate, y, res) on fp32 y: one rounding of the exact value
+            ref = torch.from_numpy(np.vectorize(orc_fma32)(gate[None, :], yo.astype(np.float32), xin.astype(np.float32)))
+            assert torch.equal(cap["x_mid"].cpu(), ref.to(torch.float32).to(torch.bfloat16))
+        else:
+            close_bf16(cap["x_mid"], xin + gate[None, :] * yo)
+        # FFN1 (+GELU glue) and FFN2 with the gated residual
+        close_bf16(cap["h2"], _ln64(f32(cap["x_mid"])))
+        q2 = _check_quant(orc, cap["h2"], cap["a2"], fm[4], H)
+        yf, _ = _gemm_ref(orc, fm[4], q2, W.layers[4], F, H)
+        gelu = 0.5 * yf * (1 + np.tanh(math.sqrt(2 / math.pi) * (yf + 0.044715 * yf ** 3)))
+        g_ = f32(cap["f"])
+        assert np.linalg.norm(g_ - gelu) <= 1e-2 * np.linalg.norm(gelu)
+        q3 = _check_quant(orc, cap["f"], cap["a3"], fm[5], F)
+        y2, exact = _gemm_ref(orc, fm[5], q3, W.layers[5], H, F)
+        gate2 = W.g2.cpu().numpy()
+        xmid = f32(cap["x_mid"])
+        if exact:
+            ref = torch.from_numpy(np.vectorize(orc_fma32)(gate2[None, :], y2.astype(np.float32), xmid.astype(np.float32)))
+            assert torch.equal(cap["x_out"].cpu(), ref.to(torch.float32).to(torch.bfloat16))
+        else:
+            close_bf16(cap["x_out"], xmid + gate2[None, :] * y2)
+        # TDC refresh on the GPU's X_in / X_out / previous delta
+        dn, sref = orc.block_stats(bits(cap["x_in"]), bits(cap["x_out"]), bits(st["delta_prev"]))
+        assert np.array_equal(bits(st["delta_new"]), dn)
+        np.testing.assert_allclose(st["stats"][:4], sref[:4], rtol=4.2e-7)
+        np.testing.assert_allclose(st["stats"][4:], sref[4:], rtol=1e-12, atol=1e-300)
+    assert n_checked >= 3
+
+
+def orc_fma32(a, b, c):
+    """fl32(a*b + c) with one rounding (exact product and sum in fp64 are exact here:
+    24-bit x 24-bit products plus a 24-bit term fit 53 bits unless exponents differ widely;
+    use fractions for safety)."""
+    from fractions import Fraction
+    v = Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c))
+    f = np.float32(float(v))
+    best = f
+    for cand in (np.nextafter(f, np.float32(np.inf)), np.nextafter(f, np.float32(-np.inf))):
+        dc, db = abs(Fraction(float(cand)) - v), abs(Fraction(float(best)) - v)
+        if dc < db or (dc == db and (int(np.float32(cand).view(np.uint32)) & 1) == 0):
+            best = cand
+    return np.float32(best)
+
+
+def test_decisions_match_oracle(run, orc):
+    """Routing (Eq. 7 + fallbacks) and TDC (Eqs. 10-11) from the GPU statistics equal
+    the oracle's decisions step by step (exemption: within 1e-6 of a threshold)."""
+    stack, steps = run
+    cfg = orc.TdcConfig(rho=stack.cfg.rho, tau=stack.cfg.tau, n_max=stack.cfg.n_max)
+    s = orc.TdcState()
+    prev_stats, prev_skipped = None, False
+    mixed = set()
+    for st in steps:
+        t = st["t"]
+        d = orc.tdc_decide(s, cfg, t)
+        near = s.n_computed >= 2 and abs(s.e_acc - cfg.tau) <= 1e-6 * cfg.tau
+        if not near:
+            assert d == st["decision"], (t, d, st["decision"], s.e_acc)
+        d = st["decision"]
+        if d == 0:
+            gamma = None if prev_stats is None else orc.gamma_from_stats(prev_stats)
+            ref = orc.route_block(gamma, stack.tau, t, prev_skipped)
+            for j, (a, b) in enumerate(zip(ref, st["fmts"])):
+                if gamma is not None and abs(gamma - stack.tau[j]) <= 1e-6 * stack.tau[j]:
+                    continue
+                assert a == b, (t, j, gamma, stack.tau[j])
+            mixed.update(st["fmts"])
+            e = orc.cosine_error_from_stats(st["stats"][4], st["stats"][5], st["stats"][6])
+            orc.tdc_update(s, cfg, t, 0, e)
+            prev_stats, prev_skipped = st["stats"], False
+        else:
+            orc.tdc_update(s, cfg, t, 1)
+            prev_stats, prev_skipped = None, True
+    assert mixed == {0, 1}, "the synthetic block should exercise both formats"
+
+
+def test_skip_output_matches_oracle(run, orc):
+    """A skipped step's output is X_in + Delta_tp exactly."""
+    stack, steps = run
+    for i, st in enumerate(steps):
+        if st["decision"] == 1:
+            ref = orc.tdc_skip(bits(st["x"]), bits(st["delta_prev"]))
+            assert np.array_equal(bits(st["out"]), ref)
