@@ -1,0 +1,88 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(CogVideoX-5B layer shapes, M = 35,552 token rows), on sampled outputs the oracle
+computes one by one: sampled rows spread over every 256-row tile band, including the
+ragged last tile; properties that hold at any size (amax, statistics) in full."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_18742_b200 import synth  # noqa: E402
+
+M = 2 * 17776
+
+
+@pytest.fixture(scope="module")
+def D():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_18742_b200 import build, dmpq
+    build.build()
+    return dmpq
+
+
+def sample_rows(m, n=12, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = set(rng.integers(0, m, n).tolist()) | {0, 127, 128, 255, m - 1, m - 129, (m // 256) * 256}
+    return sorted(r for r in rows if 0 <= r < m)
+
+
+@pytest.mark.parametrize("n,k", [(3072, 3072), (12288, 3072), (3072, 12288)])
+def test_fullsize_gemms_sampled(D, orc, n, k):
+    x = synth.dit_activation(M, k, seed=k) if k == 3072 else synth.ffn2_activation(M, k, seed=k)
+    xd = x.cuda()
+    w, b = synth.linear_weight_device(n, k, seed=n + k, device="cuda")
+    pw = D.dmpq_pack_weights(w, b)
+    amax = torch.zeros(1, device="cuda")
+    g = torch.zeros(1, device="cuda")
+    a8 = D.QuantAct.empty(D.FMT_INT8, M, k, "cuda")
+    D.dmpq_quantize_act(xd, out_i8=a8, amax_out=amax)
+    D.dmpq_global_scale(amax, 1344.0, g)
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, M, k, "cuda", g=g)
+    D.dmpq_quantize_act(xd, out_fp4=a4)
+    y8 = torch.empty(M, n, dtype=torch.bfloat16, device="cuda")
+    y4 = torch.empty(M, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a8, pw, Y=y8)
+    D.dmpq_gemm(a4, pw, Y=y4)
+    torch.cuda.synchronize()
+    xb = synth.bits(x)
+    assert amax.item() == orc.amax_bf16(xb)
+    assert g.item() == orc.global_scale(amax.item(), 1344.0)
+    wb = synth.bits(w.cpu())
+    pk = orc.pack_weights(wb)
+    assert np.array_equal(pw.i8_codes.cpu().numpy(), pk["i8_codes"])
+    assert pw.fp4_g.item() == pk["fp4_g"]
+    bias = b.cpu().numpy()
+    c8_all = a8.codes.cpu().numpy()
+    s8_all = a8.row_scale.cpu().numpy()
+    c4_all = a4.codes.cpu().numpy()
+    sf4 = orc.sf_unswizzle(a4.sf.cpu().numpy(), M, k)
+    for r in sample_rows(M):
+        c8, s8 = orc.int8_quantize(xb[r:r + 1])
+        assert np.array_equal(c8_all[r:r + 1], c8) and s8_all[r] == s8[0]
+        c4, s4 = orc.nvfp4_quantize(xb[r:r + 1], g.item())
+        assert np.array_equal(c4_all[r:r + 1], c4) and np.array_equal(sf4[r:r + 1], s4)
+        _, yr8 = orc.gemm_int8(c8, s8, pk["i8_codes"], pk["i8_scale"], bias)
+        assert torch.equal(y8[r:r + 1].cpu(), torch.from_numpy(yr8).to(torch.bfloat16)), r
+        yr4 = orc.gemm_nvfp4(c4, s4, g.item(), pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"], bias)
+        got = y4[r].float().cpu().numpy().astype(np.float64)
+        # bf16 output of an fp32-accumulated GEMM: within bf16 rounding of the fp64 reference
+        assert np.linalg.norm(got - yr4[0]) <= 4e-3 * np.linalg.norm(yr4[0]), r
+
+
+def test_fullsize_tdc(D, orc):
+    H = 3072
+    xi = synth.dit_activation(M, H, seed=1, outlier_frac=0, tail_frac=0)
+    xo = (xi.float() + 0.01 * synth.dit_activation(M, H, seed=2, outlier_frac=0, tail_frac=0).float()).to(torch.bfloat16)
+    dp = (0.01 * synth.dit_activation(M, H, seed=3, outlier_frac=0, tail_frac=0).float()).to(torch.bfloat16)
+    delta = dp.cuda()
+    stats = torch.zeros(7, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(D.tdc_workspace_bytes(M, H), dtype=torch.uint8, device="cuda")
+    D.tdc_step(1, xi.cuda(), xo.cuda(), delta, stats, ws)
+    torch.cuda.synchronize()
+    dn, st = orc.block_stats(synth.bits(xi), synth.bits(xo), synth.bits(dp))
+    assert np.array_equal(synth.bits(delta.cpu()), dn)
+    s = stats.cpu().numpy()
+    np.testing.assert_allclose(s[:4], st[:4], rtol=4.2e-7)
+    np.testing.assert_allclose(s[4:], st[4:], rtol=1e-12)
