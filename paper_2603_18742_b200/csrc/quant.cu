@@ -57,6 +57,59 @@ struct RowReduce {
     }
 };
 
+// bf16 pair (one 32-bit word) -> packed fp32x2 (exact widening)
+__device__ __forceinline__ f2 bf16x2_to_f2(uint32_t w) { return f2make(bf16lo(w), bf16hi(w)); }
+
+// |x| max over a vector of 8 bf16, in the bf16 domain (exact): max.bf16x2 on sign-cleared words
+__device__ __forceinline__ float vec_absmax(const uint4& v) {
+    uint32_t m;
+    asm("{ .reg .b32 a, b, c, d, t, u;\n\t"
+        "and.b32 a, %1, 0x7fff7fff; and.b32 b, %2, 0x7fff7fff; and.b32 c, %3, 0x7fff7fff; and.b32 d, %4, 0x7fff7fff;\n\t"
+        "max.bf16x2 t, a, b; max.bf16x2 u, c, d; max.bf16x2 %0, t, u; }"
+        : "=r"(m) : "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+    return fmaxf(bf16lo(m), bf16hi(m));
+}
+
+// 8 bf16 -> 8 E2M1 codes (4 bytes), x * rcp per element (R4)
+__device__ __forceinline__ uint32_t vec_e2m1(const uint4& v, f2 rcp2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t codes = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const f2 q = mul2(bf16x2_to_f2(w[j]), rcp2);
+        codes |= e2m1x2(f2lo(q), f2hi(q)) << (8 * j);
+    }
+    return codes;
+}
+
+// 8 bf16 -> 8 int8 codes RNE(x * rcp) with saturation (the clamp never binds).
+// cvt.pack d, a, b, c: d = {c[15:0], a, b} (bytes 3..0) -> element order i0..i3 in bytes 0..3
+__device__ __forceinline__ uint2 vec_int8(const uint4& v, f2 rcp2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t out[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const f2 q0 = mul2(bf16x2_to_f2(w[2 * h]), rcp2);
+        const f2 q1 = mul2(bf16x2_to_f2(w[2 * h + 1]), rcp2);
+        uint32_t r;
+        asm("{ .reg .s32 i0, i1, i2, i3; .reg .b32 p;\n\t"
+            "cvt.rni.s32.f32 i0, %1; cvt.rni.s32.f32 i1, %2; cvt.rni.s32.f32 i2, %3; cvt.rni.s32.f32 i3, %4;\n\t"
+            "cvt.pack.sat.s8.s32.b32 p, i3, i2, 0; cvt.pack.sat.s8.s32.b32 %0, i1, i0, p; }"
+            : "=r"(r) : "f"(f2lo(q0)), "f"(f2hi(q0)), "f"(f2lo(q1)), "f"(f2hi(q1)));
+        out[h] = r;
+    }
+    return make_uint2(out[0], out[1]);
+}
+
+template <int NV>
+__device__ __forceinline__ void load_row(uint4 (&v)[NV], const uint16_t* xr, int tid, int tpr, int nvec, bool valid) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int vi = tid + i * tpr;
+        v[i] = (valid && vi < nvec) ? ldg_stream(xr + (size_t)vi * 8) : make_uint4(0, 0, 0, 0);
+    }
+}
+
 template <int NV, bool WARP_ROW>
 __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
     __shared__ float red[40];
@@ -70,70 +123,65 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
     const bool want_fp4 = p.fp4_codes != nullptr;
     const bool want_i8 = p.i8_codes != nullptr;
     const float g = want_fp4 ? *p.g : 1.0f;
+    const int stride = gridDim.x * rows_per_cta;
     float cta_amax = 0.0f;
 
-    for (int row = blockIdx.x * rows_per_cta + row_slot; row < p.m; row += gridDim.x * rows_per_cta) {
-        const uint16_t* xr = p.X + (size_t)row * p.ldx;
-        uint4 v[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = tid + i * tpr;
-            v[i] = (vi < nvec) ? ldg_stream(xr + (size_t)vi * 8) : make_uint4(0, 0, 0, 0);
-        }
+    int row = blockIdx.x * rows_per_cta + row_slot;
+    uint4 v[NV];
+    load_row<NV>(v, p.X + (size_t)row * p.ldx, tid, tpr, nvec, row < p.m);
+    // WARP_ROW warps run independent row sequences; CTA rows iterate uniformly
+    while (WARP_ROW ? (row < p.m) : (row < p.m)) {
+        const int next = row + stride;
+        uint4 nv[NV];   // prefetch the next row while this one is processed
+        load_row<NV>(nv, p.X + (size_t)next * p.ldx, tid, tpr, nvec, next < p.m);
         if (p.flags & DMPQ_QF_LAYERNORM) {
-            // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue)
-            float s = 0.0f;
+            // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue, R13)
+            f2 s2 = f2make(0.0f, 0.0f);
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
-                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) s = __fadd_rn(__fadd_rn(s, bf16lo(w[j])), bf16hi(w[j]));
+                s2 = add2(s2, add2(bf16x2_to_f2(v[i].x), bf16x2_to_f2(v[i].y)));
+                s2 = add2(s2, add2(bf16x2_to_f2(v[i].z), bf16x2_to_f2(v[i].w)));
             }
-            const float mean = __fdiv_rn(rr.sum(s), (float)p.k);
-            float q = 0.0f;
+            const float mean = __fdiv_rn(rr.sum(__fadd_rn(f2lo(s2), f2hi(s2))), (float)p.k);
+            const f2 mean2 = f2make(mean, mean);
+            f2 q2 = f2make(0.0f, 0.0f);
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
-                const int vi = tid + i * tpr;
-                if (vi >= nvec) continue;
+                if (tid + i * tpr >= nvec) continue;
                 const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const float a = __fsub_rn(bf16lo(w[j]), mean), b = __fsub_rn(bf16hi(w[j]), mean);
-                    q = __fadd_rn(q, __fadd_rn(__fmul_rn(a, a), __fmul_rn(b, b)));
+                    const f2 d = add2(bf16x2_to_f2(w[j]), f2make(-mean, -mean));
+                    q2 = add2(q2, mul2(d, d));
                 }
             }
-            const float var = __fdiv_rn(rr.sum(q), (float)p.k);
+            const float var = __fdiv_rn(rr.sum(__fadd_rn(f2lo(q2), f2hi(q2))), (float)p.k);
             const float rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps)));
+            const f2 rstd2 = f2make(rstd, rstd);
+            (void)mean2;
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 const int vi = tid + i * tpr;
                 uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    w[j] = pack_bf16x2(__fmul_rn(__fsub_rn(bf16lo(w[j]), mean), rstd),
-                                       __fmul_rn(__fsub_rn(bf16hi(w[j]), mean), rstd));
+                    w[j] = pack_bf16x2_f2(mul2(add2(bf16x2_to_f2(w[j]), f2make(-mean, -mean)), rstd2));
                 v[i] = (vi < nvec) ? make_uint4(w[0], w[1], w[2], w[3]) : make_uint4(0, 0, 0, 0);
                 if ((p.flags & DMPQ_QF_WRITE_H) && vi < nvec)
                     *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)vi * 8) = v[i];
             }
         }
-        // per-vector |x| maxima
         float vmax[NV];
         float tmax = 0.0f;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-            float mx = 0.0f;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) mx = fmaxf(mx, fmaxf(fabsf(bf16lo(w[j])), fabsf(bf16hi(w[j]))));
-            vmax[i] = mx;
-            tmax = fmaxf(tmax, mx);
+            vmax[i] = vec_absmax(v[i]);
+            tmax = fmaxf(tmax, vmax[i]);
         }
         cta_amax = fmaxf(cta_amax, tmax);
 
         if (want_fp4) {
-            const int rt = row >> 7;
-            uint8_t* sf_row = p.fp4_sf + (size_t)rt * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
+            uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 const int vi = tid + i * tpr;
@@ -143,11 +191,7 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
                 const uint32_t sb = e4m3_rn_satfinite(raw);
                 const float eff = __fmul_rn(e4m3_decode(sb), g);
                 const float rcp = eff > 0.0f ? __frcp_rn(eff) : 0.0f;
-                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-                uint32_t codes = 0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    codes |= e2m1x2(__fmul_rn(bf16lo(w[j]), rcp), __fmul_rn(bf16hi(w[j]), rcp)) << (8 * j);
+                const uint32_t codes = vec_e2m1(v[i], f2make(rcp, rcp));
                 // gather the 4 block scales of this 64-element group (lanes 8q, 8q+2, 8q+4, 8q+6)
                 const int base = lane & ~7;
                 const uint32_t s0 = __shfl_sync(0xffffffffu, sb, base + 0);
@@ -156,10 +200,8 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
                 const uint32_t s3 = __shfl_sync(0xffffffffu, sb, base + 6);
                 if (vi < nvec) {
                     *reinterpret_cast<uint32_t*>(p.fp4_codes + (size_t)row * (p.k >> 1) + (size_t)vi * 4) = codes;
-                    if ((lane & 7) == 0) {
-                        const int c4 = vi >> 3;  // scale-column atom (4 scales = 64 elements)
-                        *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
-                    }
+                    if ((lane & 7) == 0)
+                        *reinterpret_cast<uint32_t*>(sf_row + (size_t)(vi >> 3) * 512) = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
                 }
             }
         }
@@ -167,29 +209,17 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
             const float a = rr.max(tmax);
             const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
             if (tid == 0) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+            const f2 rcp2 = f2make(rcp, rcp);
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 const int vi = tid + i * tpr;
-                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-                uint32_t out[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t packed = 0;
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const uint32_t ww = w[2 * h + j];
-                        int c0 = __float2int_rn(__fmul_rn(bf16lo(ww), rcp));
-                        int c1 = __float2int_rn(__fmul_rn(bf16hi(ww), rcp));
-                        c0 = max(-128, min(127, c0));
-                        c1 = max(-128, min(127, c1));
-                        packed |= ((uint32_t)(c0 & 0xFF) | ((uint32_t)(c1 & 0xFF) << 8)) << (16 * j);
-                    }
-                    out[h] = packed;
-                }
-                if (vi < nvec)
-                    *reinterpret_cast<uint2*>(p.i8_codes + (size_t)row * p.k + (size_t)vi * 8) = make_uint2(out[0], out[1]);
+                const uint2 c = vec_int8(v[i], rcp2);
+                if (vi < nvec) *reinterpret_cast<uint2*>(p.i8_codes + (size_t)row * p.k + (size_t)vi * 8) = c;
             }
         }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = nv[i];
+        row = next;
     }
     // zero the scale rows that pad m up to a multiple of 128 (read by the GEMM's M tail)
     if (want_fp4) {
@@ -197,14 +227,14 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
         const int words_per_row = p.kc4;  // one 32-bit word per (row, atom)
         for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < pad_rows * words_per_row;
              idx += gridDim.x * blockDim.x) {
-            const int row = p.m + idx / words_per_row, c4 = idx % words_per_row;
-            uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
+            const int r = p.m + idx / words_per_row, c4 = idx % words_per_row;
+            uint8_t* sf_row = p.fp4_sf + (size_t)(r >> 7) * p.kc4 * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4;
             *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = 0u;
         }
     }
     if (p.amax_out) {
-        float a = warp_max(cta_amax);
-        if (lane == 0) atomic_max_nonneg(p.amax_out, a);
+        float am = warp_max(cta_amax);
+        if (lane == 0) atomic_max_nonneg(p.amax_out, am);
     }
 }
 
