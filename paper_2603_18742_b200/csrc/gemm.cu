@@ -132,7 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         int stage = 0;
         uint32_t phase = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl) {
-            const int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
+            const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int m0 = mt * 256 + (int)rank * BM;
             const int nb0 = nt * BN + (int)rank * (BN / 2);
             for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -167,7 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             if constexpr (FP4) idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
             else idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
             for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
-                const int nt = tile / p.num_m_tiles;
+                const int nt = tile % p.num_n_tiles;
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 // SFB rows start at the 128-row atom below n0; BN=192 odd tiles start 64 rows (2 columns) in
@@ -229,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
         const bool has_res = (p.flags & DMPQ_EP_RESIDUAL) != 0;
         for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
-            const int mt = tile % p.num_m_tiles, nt = tile / p.num_m_tiles;
+            const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int n0 = nt * BN;
