@@ -92,9 +92,16 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        return dist.get_rank(), world, local, dist.group.WORLD
+        # DMPQ_DEVICE_MAP=shared puts every rank on GPU 0 (functional test of the multi-rank
+        # path on a 1-GPU box, with DMPQ_DIST_BACKEND=gloo); the contract run uses one GPU per rank.
+        dev_index = 0 if os.environ.get("DMPQ_DEVICE_MAP") == "shared" else local
+        torch.cuda.set_device(dev_index)
+        backend = os.environ.get("DMPQ_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+        return dist.get_rank(), world, dev_index, dist.group.WORLD
     return 0, 1, 0, None
 
 
@@ -230,6 +237,13 @@ def run_ours(args):
     gemm_t = model.gemm_time_s()
     gemm_flops = dict(model.gemm_flops)
     model.timing = False
+
+    # every rank must have taken identical TDC/routing decisions
+    sig = float(sum((i + 1) * (2 + d + sum(f or [])) for r in recs for i, (d, f) in enumerate(zip(r.decisions, r.fmts))))
+    if group is not None:
+        s = torch.tensor([sig, -sig], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(s, op=torch.distributed.ReduceOp.MAX, group=group)
+        assert float(s[0]) == sig and float(s[1]) == -sig, "ranks disagree on the per-step decisions"
 
     tt = torch.tensor([elapsed, local_flops], dtype=torch.float64, device=dev)
     if group is not None:
