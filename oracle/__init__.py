@@ -69,6 +69,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_global_scale.argtypes, L.oracle_global_scale.restype = [F, F], F
         L.oracle_sf_offset.argtypes, L.oracle_sf_offset.restype = [I, I, I], LL
         L.oracle_int8_quantize_rows.argtypes = [P, I, I, I, P, P]
+        L.oracle_fht128_f32.argtypes = [P, P, LL]
+        L.oracle_nvfp4_quantize_f32.argtypes = [P, I, I, F, P, P]
+        L.oracle_int8_quantize_rows_f32.argtypes = [P, I, I, P, P]
+        L.oracle_pack_weights_hadamard.argtypes = [P, I, I, P, P, P, P, P, P]
         L.oracle_pack_weights.argtypes = [P, I, I, P, P, P, P, P]
         L.oracle_gemm_int8.argtypes, L.oracle_gemm_int8.restype = [P, P, P, P, P, I, I, I, I, I, P, P], I
         L.oracle_gemm_nvfp4.argtypes = [P, P, F, P, P, F, P, I, I, I, I, I, P]
@@ -201,6 +205,52 @@ def pack_weights(w_bf16: np.ndarray):
     )
     lib().oracle_pack_weights(_p(w), n, k, _p(out["fp4_codes"]), _p(out["fp4_sf"]), _p(out["fp4_g"]),
                               _p(out["i8_codes"]), _p(out["i8_scale"]))
+    out["fp4_g"] = float(out["fp4_g"][0])
+    return out
+
+
+def fht128(x) -> np.ndarray:
+    """Normalized Sylvester block Hadamard over 128-element blocks of the last axis
+    (reading R14), fp32 butterflies in the fixed stage order."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    assert x.shape[-1] % 128 == 0
+    y = np.empty_like(x)
+    lib().oracle_fht128_f32(_p(x), _p(y), x.size)
+    return y
+
+
+def nvfp4_quantize_f32(x32: np.ndarray, g: float):
+    x = np.ascontiguousarray(x32, dtype=np.float32)
+    m, k = x.shape
+    codes = np.zeros((m, k // 2), dtype=np.uint8)
+    sf = np.zeros((m, k // 16), dtype=np.uint8)
+    lib().oracle_nvfp4_quantize_f32(_p(x), m, k, float(g), _p(codes), _p(sf))
+    return codes, sf
+
+
+def int8_quantize_f32(x32: np.ndarray):
+    x = np.ascontiguousarray(x32, dtype=np.float32)
+    m, k = x.shape
+    codes = np.zeros((m, k), dtype=np.int8)
+    scale = np.zeros(m, dtype=np.float32)
+    lib().oracle_int8_quantize_rows_f32(_p(x), m, k, _p(codes), _p(scale))
+    return codes, scale
+
+
+def pack_weights_hadamard(w_bf16: np.ndarray):
+    """Weight pack with the offline block-Hadamard rotation of every row (R14)."""
+    w = _u16(w_bf16)
+    n, k = w.shape
+    out = dict(
+        fp4_codes=np.zeros((n, k // 2), dtype=np.uint8),
+        fp4_sf=np.zeros((n, k // 16), dtype=np.uint8),
+        fp4_g=np.zeros(1, dtype=np.float32),
+        i8_codes=np.zeros((n, k), dtype=np.int8),
+        i8_scale=np.zeros(n, dtype=np.float32),
+    )
+    scratch = np.zeros((n, k), dtype=np.float32)
+    lib().oracle_pack_weights_hadamard(_p(w), n, k, _p(out["fp4_codes"]), _p(out["fp4_sf"]), _p(out["fp4_g"]),
+                                       _p(out["i8_codes"]), _p(out["i8_scale"]), _p(scratch))
     out["fp4_g"] = float(out["fp4_g"][0])
     return out
 

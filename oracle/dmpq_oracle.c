@@ -191,6 +191,77 @@ long long oracle_sf_offset(int r, int c, int k) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* Online block Hadamard smoothing ("we apply a Fast Hadamard Transform  */
+/* (FHT) over local activation blocks (B=128)").  Reading R14: the   */
+/* normalized Sylvester-ordered transform y = H_128 x / sqrt(128) per 128-block, */
+/* evaluated as the fast transform in FP32 exactly in this order: stages        */
+/* h = 1, 2, 4, ..., 64; within a stage every pair (i, i+h) with (i & h) == 0   */
+/* becomes (fl(a + b), fl(a - b)); then every element is multiplied by          */
+/* fl32(1/sqrt(128)).                                                            */
+/* ------------------------------------------------------------------------ */
+
+void oracle_fht128_f32(const float* x, float* y, long long n) {
+    const float s = (float)(1.0 / sqrt(128.0));
+    for (long long b0 = 0; b0 < n; b0 += 128) {
+        float v[128];
+        for (int i = 0; i < 128; ++i) v[i] = x[b0 + i];
+        for (int h = 1; h < 128; h <<= 1)
+            for (int i = 0; i < 128; ++i)
+                if ((i & h) == 0) {
+                    float a = v[i], b = v[i + h];
+                    v[i] = a + b;
+                    v[i + h] = a - b;
+                }
+        for (int i = 0; i < 128; ++i) y[b0 + i] = v[i] * s;
+    }
+}
+
+/* NVFP4 quantization of FP32 rows (the Hadamard-smoothed path): identical steps to
+ * oracle_nvfp4_quantize, the inputs being fp32 values instead of bf16 ones. */
+void oracle_nvfp4_quantize_f32(const float* x, int m, int k, float g, uint8_t* codes, uint8_t* sf) {
+    for (int r = 0; r < m; ++r) {
+        for (int b = 0; b < k / 16; ++b) {
+            const float* xb = x + (size_t)r * k + (size_t)b * 16;
+            float a_b = 0.0f;
+            for (int i = 0; i < 16; ++i)
+                if (fabsf(xb[i]) > a_b) a_b = fabsf(xb[i]);
+            float raw = (a_b / 6.0f) / g;
+            uint8_t s_b = oracle_e4m3_encode_nonneg(raw);
+            float eff = (float)oracle_e4m3_decode(s_b) * g;
+            float rcp = eff > 0.0f ? 1.0f / eff : 0.0f;
+            sf[(size_t)r * (k / 16) + b] = s_b;
+            for (int i = 0; i < 16; i += 2) {
+                uint8_t c0 = oracle_e2m1_encode(xb[i] * rcp), c1 = oracle_e2m1_encode(xb[i + 1] * rcp);
+                codes[(size_t)r * (k / 2) + (size_t)b * 8 + i / 2] = (uint8_t)(c0 | (c1 << 4));
+            }
+        }
+    }
+}
+
+/* Per-token symmetric INT8 of FP32 rows (same steps as oracle_int8_quantize_rows). */
+void oracle_int8_quantize_rows_f32(const float* x, int m, int k, int8_t* codes, float* scale) {
+    for (int r = 0; r < m; ++r) {
+        const float* xr = x + (size_t)r * k;
+        float a = 0.0f;
+        for (int j = 0; j < k; ++j)
+            if (fabsf(xr[j]) > a) a = fabsf(xr[j]);
+        if (a == 0.0f) {
+            scale[r] = 1.0f;
+            for (int j = 0; j < k; ++j) codes[(size_t)r * k + j] = 0;
+            continue;
+        }
+        scale[r] = a / 127.0f;
+        float rcp = 127.0f / a;
+        for (int j = 0; j < k; ++j) {
+            double rq = nearbyint((double)(xr[j] * rcp));
+            if (rq > 127.0) rq = 127.0;
+            if (rq < -128.0) rq = -128.0;
+            codes[(size_t)r * k + j] = (int8_t)rq;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Symmetric INT8: "maps values to [-128, 127] with s = max(|X|)/127",  */
 /* Eq. 1 with z = 0: X_q = clip(round(X/s), -128, 127).  Granularity: one scale */
 /* per token (row), reading R2.  X/s evaluated as fl(x * fl(127/a)) (R4);       */
@@ -271,6 +342,36 @@ void oracle_pack_weights(const uint16_t* w, int n, int k,
             i8_codes[(size_t)r * k + j] = (int8_t)rq;
         }
     }
+}
+
+/* Weight pack with the offline Hadamard rotation (reading R14): every row of W
+ * (nn.Linear [n x k]) gets the same block FHT along k as the activations, so
+ * (H x) . (H w) = x . w; then the two packed forms of oracle_pack_weights from the
+ * rotated FP32 weights (g_w from their amax). */
+void oracle_pack_weights_hadamard(const uint16_t* w, int n, int k,
+                                  uint8_t* fp4_codes, uint8_t* fp4_sf, float* fp4_g,
+                                  int8_t* i8_codes, float* i8_scale, float* w_rot /* [n x k] scratch/out */) {
+    for (size_t i = 0; i < (size_t)n * k; ++i) w_rot[i] = oracle_bf16_to_f32(w[i]);
+    oracle_fht128_f32(w_rot, w_rot, (long long)n * k);
+    float amax = 0.0f;
+    for (size_t i = 0; i < (size_t)n * k; ++i)
+        if (fabsf(w_rot[i]) > amax) amax = fabsf(w_rot[i]);
+    float g = oracle_global_scale(amax, 2688.0f);
+    *fp4_g = g;
+    oracle_nvfp4_quantize_f32(w_rot, n, k, g, fp4_codes, fp4_sf);
+    for (int r = 0; r < n; ++r) {
+        float a = 0.0f;
+        float* wr = w_rot + (size_t)r * k;  /* reuse the scratch for W^ of this row */
+        for (int j = 0; j < k; ++j) {
+            uint8_t byte = fp4_codes[(size_t)r * (k / 2) + j / 2];
+            uint8_t nib = (j & 1) ? (byte >> 4) : (byte & 15);
+            float eff = (float)oracle_e4m3_decode(fp4_sf[(size_t)r * (k / 16) + j / 16]) * g;
+            wr[j] = (float)oracle_e2m1_decode(nib) * eff;
+            if (fabsf(wr[j]) > a) a = fabsf(wr[j]);
+        }
+        (void)a;
+    }
+    oracle_int8_quantize_rows_f32(w_rot, n, k, i8_codes, i8_scale);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -428,3 +428,84 @@ def test_tdc_properties(orc):
             run = run + 1 if s else 0
             best = max(best, run)
         assert best <= n_max
+
+
+# ---------------------------------------------------------------------------- block Hadamard (R14)
+
+def _sylvester(n):
+    h = np.array([[1.0]])
+    while h.shape[0] < n:
+        h = np.block([[h, h], [h, -h]])
+    return h
+
+
+def test_fht_one_hot_is_a_hadamard_row(orc):
+    """Sylvester H[i][j] = (-1)^popcount(i & j); a one-hot block maps to +-1/sqrt(128)
+    exactly (every butterfly adds a value to zero)."""
+    s = np.float32(1.0 / np.sqrt(128.0))
+    for j in (0, 1, 5, 64, 127):
+        x = np.zeros((1, 128), np.float32)
+        x[0, j] = 1.0
+        y = orc.fht128(x)[0]
+        ref = np.array([(-1.0) ** bin(i & j).count("1") for i in range(128)], np.float32) * s
+        assert np.array_equal(y, ref)
+
+
+def test_fht_matches_dense_transform_and_is_an_involution(orc):
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((6, 384)).astype(np.float32)
+    x[:, 7] *= 80.0
+    y = orc.fht128(x)
+    H = _sylvester(128) / np.sqrt(128.0)
+    dense = (x.astype(np.float64).reshape(6, 3, 128) @ H.T).reshape(6, 384)
+    assert np.max(np.abs(y - dense)) <= 1e-5 * np.max(np.abs(dense))
+    np.testing.assert_allclose(np.linalg.norm(y, axis=1), np.linalg.norm(x.astype(np.float64), axis=1), rtol=1e-6)
+    assert np.max(np.abs(orc.fht128(y) - x)) <= 1e-5 * np.max(np.abs(x))          # S:209 involution
+    # linear-layer transparency (S:219): (Hx).(Hw) == x.w
+    w = rng.standard_normal((4, 384)).astype(np.float32)
+    np.testing.assert_allclose(orc.fht128(x).astype(np.float64) @ orc.fht128(w).T.astype(np.float64),
+                               x.astype(np.float64) @ w.T.astype(np.float64), rtol=1e-5, atol=1e-4)
+
+
+def test_fht_smooths_channel_outliers_for_int8(orc):
+    """P:187 / S:220: block-Hadamard smoothing redistributes activation outliers; with
+    a few large outlier channels, the per-token INT8 error (scale set by the row max)
+    drops after the rotation (the error is measured back in the original basis)."""
+    rng = np.random.default_rng(22)
+    e_plain, e_fht = [], []
+    for trial in range(40):
+        x = rng.standard_normal((4, 256)).astype(np.float32)
+        x[:, rng.integers(0, 256, 2)] *= 60.0
+        xb = torch.tensor(x).to(torch.bfloat16).float().numpy()
+        c, s = orc.int8_quantize_f32(xb)
+        e_plain.append(np.linalg.norm(c * s[:, None] - xb) / np.linalg.norm(xb))
+        y = orc.fht128(xb)
+        c2, s2 = orc.int8_quantize_f32(y)
+        back = orc.fht128((c2 * s2[:, None]).astype(np.float32))
+        e_fht.append(np.linalg.norm(back - xb) / np.linalg.norm(xb))
+    assert np.mean(e_fht) < 0.5 * np.mean(e_plain)
+
+
+def test_f32_quantizers_agree_with_bf16_ones_on_bf16_values(orc):
+    rng = np.random.default_rng(23)
+    x = torch.tensor(rng.standard_normal((5, 128)).astype(np.float32)).to(torch.bfloat16)
+    xb, xf = bf16_bits(x.float().numpy()), x.float().numpy()
+    c1, s1 = orc.nvfp4_quantize(xb, 0.01)
+    c2, s2 = orc.nvfp4_quantize_f32(xf, 0.01)
+    assert np.array_equal(c1, c2) and np.array_equal(s1, s2)
+    i1, t1 = orc.int8_quantize(xb)
+    i2, t2 = orc.int8_quantize_f32(xf)
+    assert np.array_equal(i1, i2) and np.array_equal(t1, t2)
+
+
+def test_pack_weights_hadamard(orc):
+    rng = np.random.default_rng(24)
+    w = bf16_bits((rng.standard_normal((32, 256)) / 16).astype(np.float32))
+    pk = orc.pack_weights_hadamard(w)
+    wr = orc.fht128(bf16_vals(w))
+    assert pk["fp4_g"] == orc.global_scale(float(np.abs(wr).max()), 2688.0)
+    c, s = orc.nvfp4_quantize_f32(wr, pk["fp4_g"])
+    assert np.array_equal(c, pk["fp4_codes"]) and np.array_equal(s, pk["fp4_sf"])
+    what = orc.nvfp4_dequantize(pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"])
+    err = np.abs(what - pk["i8_codes"] * pk["i8_scale"][:, None].astype(np.float64))
+    assert np.all(err <= pk["i8_scale"][:, None] * (0.5 + 1e-5))
