@@ -187,7 +187,7 @@ def run_ours(args):
     T = max(T, args.warmup + args.steps)
     peaks, peak_kind = load_peaks()
 
-    model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group)
+    model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard)
     # block-0 input trajectory basis (this rank's rows)
     A, B = synth.trajectory_basis(m, H, seed=1000 + rank, device=dev)
 
@@ -339,6 +339,7 @@ def run_ours(args):
         "config": {"workload": desc, "blocks": nb, "hidden": H, "ffn": F, "tokens_total": M, "tokens_per_rank": m,
                    "timesteps": list(range(args.warmup, args.warmup + args.steps)), "T": T,
                    "parallelism": f"token-shard x{world}", "l2": "inputs larger than L2 (multi-GB working set per step)",
+                   "hadamard": not args.no_hadamard,
                    "mix": mix},
         "block_step_ms": elapsed / args.steps / nb * 1e3,
         "effective_tflops_dense_equiv": dense_flops / elapsed / 1e12,
@@ -365,6 +366,7 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override the block count (development only)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs --warmup >= 3", file=sys.stderr)

@@ -112,6 +112,13 @@ typedef struct {
  * Shapes: k % 64 == 0, n % 16 == 0, n, k > 0. */
 dmpq_status dmpq_pack_weights(const uint16_t* W, int n, int k, dmpq_weights* out, dmpq_stream_t s);
 
+#define DMPQ_PACK_HADAMARD 1u  /* rotate every row by the block FHT first (offline half of P:187's smoothing, R14) */
+
+/* dmpq_pack_weights with options: DMPQ_PACK_HADAMARD packs W~ = W . blockdiag(H_128)/sqrt(128)
+ * (g_w from amax(W~)), so (H x) . W~^T = x . W^T for activations quantised with
+ * DMPQ_QF_HADAMARD. k % 128 == 0 then. */
+dmpq_status dmpq_pack_weights_ex(const uint16_t* W, int n, int k, uint32_t flags, dmpq_weights* out, dmpq_stream_t s);
+
 /* ========================================================================== */
 /* 2. dmpq_predict  (host-pure)                                               */
 /* ========================================================================== */
@@ -152,7 +159,9 @@ dmpq_status dmpq_predict(const dmpq_block_stats* st, const double* tau_gamma, in
 /* ========================================================================== */
 
 #define DMPQ_QF_LAYERNORM 1u  /* normalise each row first: h = (x - mean)/sqrt(var + eps), no affine (block glue) */
-#define DMPQ_QF_WRITE_H   2u  /* also store the bf16 values that were quantised into h_out */
+#define DMPQ_QF_WRITE_H   2u  /* also store the bf16 values that were quantised into h_out (before any rotation) */
+#define DMPQ_QF_HADAMARD  4u  /* rotate every 128-element block by the normalized Sylvester FHT before quantising
+                                 (P:187 online block Hadamard, R14); pair with weights packed with DMPQ_PACK_HADAMARD */
 
 typedef struct {
     uint32_t flags;
@@ -174,7 +183,9 @@ typedef struct {
  *  amax_out: if non-NULL, device FP32 that receives max(*amax_out, max|x|)
  *  (atomic; the caller zeroes it once per step). With DMPQ_QF_LAYERNORM the
  *  quantised (and amax'd) values are the bf16-rounded normalised rows.
- *  Shapes: k % 64 == 0, 0 < k <= 16384, m >= 0 (m == 0 is a no-op). */
+ *  With DMPQ_QF_HADAMARD the values quantised (and amax'd) are the FP32 FHT outputs
+ *  y = H_128 x / sqrt(128) per 128-block, butterflies h = 1..64 in FP32 (R14).
+ *  Shapes: k % 64 == 0 (k % 128 == 0 with DMPQ_QF_HADAMARD), 0 < k <= 16384, m >= 0. */
 dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
                               dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s);
 

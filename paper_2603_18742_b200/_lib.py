@@ -19,7 +19,8 @@ DMPQ_OK, DMPQ_EINVAL, DMPQ_ESHAPE, DMPQ_EALIGN, DMPQ_EZERONORM, DMPQ_ECUDA, DMPQ
 STATUS_NAMES = ["DMPQ_OK", "DMPQ_EINVAL", "DMPQ_ESHAPE", "DMPQ_EALIGN", "DMPQ_EZERONORM", "DMPQ_ECUDA",
                 "DMPQ_EUNSUPPORTED"]
 FMT_INT8, FMT_NVFP4 = 0, 1
-QF_LAYERNORM, QF_WRITE_H = 1, 2
+QF_LAYERNORM, QF_WRITE_H, QF_HADAMARD = 1, 2, 4
+PACK_HADAMARD = 1
 EP_BIAS, EP_GELU_TANH, EP_RESIDUAL = 1, 2, 4
 TDC_SKIP, TDC_REFRESH = 0, 1
 TDC_COMPUTE, TDC_DECIDE_SKIP = 0, 1
@@ -72,6 +73,7 @@ _SIGNATURES = {
     "dmpq_sf_bytes": ([c_int, c_int], c_size_t),
     "tdc_workspace_bytes": ([c_int, c_int], c_size_t),
     "dmpq_pack_weights": ([c_void_p, c_int, c_int, ctypes.POINTER(Weights), c_void_p], c_int),
+    "dmpq_pack_weights_ex": ([c_void_p, c_int, c_int, c_uint32, ctypes.POINTER(Weights), c_void_p], c_int),
     "dmpq_derive_tau": ([c_double, c_double, c_double, c_double], c_double),
     "dmpq_predict": ([ctypes.POINTER(BlockStats), ctypes.POINTER(c_double), c_int, c_int, c_int, c_int,
                       ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(c_double)], c_int),

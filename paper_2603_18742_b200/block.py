@@ -56,7 +56,7 @@ class BlockWeights:
         return sum(w.nbytes() for w in self.layers)
 
 
-def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float) -> BlockWeights:
+def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, hadamard: bool = False) -> BlockWeights:
     shapes = [(H, H), (H, H), (H, H), (H, H), (F, H), (H, F)]
     layers = []
     for j, (n, k) in enumerate(shapes):
@@ -64,7 +64,7 @@ def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float) -> 
             w, b = synth.linear_weight_device(n, k, seed * 16 + j, device)
         else:
             w, b = synth.linear_weight(n, k, seed * 16 + j)
-        layers.append(D.dmpq_pack_weights(w.to(device), b.to(device)))
+        layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard))
         del w
     g = torch.Generator(device="cpu")
     g.manual_seed(seed * 16 + 15)
@@ -113,7 +113,7 @@ class DiTStack:
 
     def __init__(self, n_blocks: int, H: int, F: int, m_local: int, device, seed: int = 0,
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
-                 force_fmt: int | None = None, group=None):
+                 force_fmt: int | None = None, group=None, hadamard: bool = False):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -121,9 +121,11 @@ class DiTStack:
         self.tdc_enabled = tdc_enabled
         self.force_fmt = force_fmt
         self.group = group
+        self.hadamard = hadamard      # online block-Hadamard smoothing (R14)
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
-        self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b]) for b in range(n_blocks)]
+        self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard)
+                       for b in range(n_blocks)]
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
         self.amax = torch.zeros(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
         self.ws = Workspace(m_local, H, F, self.device, self.g_table)
@@ -166,7 +168,8 @@ class DiTStack:
         a0_f4 = ws.act(0, D.FMT_NVFP4, b) if D.FMT_NVFP4 in need else None
         cap = self.capture is not None
         h1 = torch.empty(m, H, dtype=torch.bfloat16, device=x_in.device) if cap else None
-        D.dmpq_quantize_act(x_in, out_i8=a0_i8, out_fp4=a0_f4, amax_out=amax[0:1], layernorm=True, h_out=h1)
+        hd = self.hadamard
+        D.dmpq_quantize_act(x_in, out_i8=a0_i8, out_fp4=a0_f4, amax_out=amax[0:1], layernorm=True, h_out=h1, hadamard=hd)
         if cap:
             self._cap("x_in", x_in); self._cap("h1", h1)
             self._cap_act("a0_i8", a0_i8); self._cap_act("a0_f4", a0_f4)
@@ -176,7 +179,8 @@ class DiTStack:
             self._cap(f"y{j}", out)
         # O projection on the attention stand-in a = v, gated residual in the epilogue
         a1 = ws.act(1, fmts[3], b)
-        D.dmpq_quantize_act(ws.v, **{("out_i8" if fmts[3] == D.FMT_INT8 else "out_fp4"): a1}, amax_out=amax[1:2])
+        D.dmpq_quantize_act(ws.v, **{("out_i8" if fmts[3] == D.FMT_INT8 else "out_fp4"): a1}, amax_out=amax[1:2],
+                            hadamard=hd)
         self._cap_act("a1", a1)
         self._gemm(a1, W.layers[3], Y=ws.x_mid, residual=x_in, gate=W.g1)
         self._cap("x_mid", ws.x_mid)
@@ -184,13 +188,14 @@ class DiTStack:
         a2 = ws.act(2, fmts[4], b)
         h2 = torch.empty(m, H, dtype=torch.bfloat16, device=x_in.device) if cap else None
         D.dmpq_quantize_act(ws.x_mid, **{("out_i8" if fmts[4] == D.FMT_INT8 else "out_fp4"): a2},
-                            amax_out=amax[2:3], layernorm=True, h_out=h2)
+                            amax_out=amax[2:3], layernorm=True, h_out=h2, hadamard=hd)
         if cap:
             self._cap("h2", h2); self._cap_act("a2", a2)
         self._gemm(a2, W.layers[4], Y=ws.f, gelu=True)
         self._cap("f", ws.f)
         a3 = ws.act(3, fmts[5], b)
-        D.dmpq_quantize_act(ws.f, **{("out_i8" if fmts[5] == D.FMT_INT8 else "out_fp4"): a3}, amax_out=amax[3:4])
+        D.dmpq_quantize_act(ws.f, **{("out_i8" if fmts[5] == D.FMT_INT8 else "out_fp4"): a3}, amax_out=amax[3:4],
+                            hadamard=hd)
         self._cap_act("a3", a3)
         self._gemm(a3, W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
         self._cap("x_out", x_out)

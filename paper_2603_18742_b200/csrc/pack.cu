@@ -62,7 +62,15 @@ __global__ void __launch_bounds__(256) pack_int8_from_fp4_kernel(const uint8_t* 
 using namespace dmpq;
 
 extern "C" dmpq_status dmpq_pack_weights(const uint16_t* W, int n, int k, dmpq_weights* out, dmpq_stream_t s) {
+    return dmpq_pack_weights_ex(W, n, k, 0u, out, s);
+}
+
+extern "C" dmpq_status dmpq_pack_weights_ex(const uint16_t* W, int n, int k, uint32_t flags, dmpq_weights* out,
+                                            dmpq_stream_t s) {
     DMPQ_REQUIRE(W && out, DMPQ_EINVAL, "dmpq_pack_weights: NULL argument");
+    DMPQ_REQUIRE((flags & ~DMPQ_PACK_HADAMARD) == 0, DMPQ_EINVAL, "dmpq_pack_weights: unknown flags 0x%x", flags);
+    const bool had = (flags & DMPQ_PACK_HADAMARD) != 0;
+    DMPQ_REQUIRE(!had || k % 128 == 0, DMPQ_ESHAPE, "dmpq_pack_weights: DMPQ_PACK_HADAMARD needs k %% 128 == 0");
     DMPQ_REQUIRE(n > 0 && k > 0 && k % 64 == 0 && n % 16 == 0 && k <= 16384, DMPQ_ESHAPE,
                  "dmpq_pack_weights: need n %% 16 == 0, k %% 64 == 0, k <= 16384 (n=%d k=%d)", n, k);
     DMPQ_REQUIRE(out->n == n && out->k == k, DMPQ_ESHAPE, "dmpq_pack_weights: out->n/k mismatch");
@@ -72,17 +80,32 @@ extern "C" dmpq_status dmpq_pack_weights(const uint16_t* W, int n, int k, dmpq_w
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_pack_weights: needs an sm_100 device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
     if (cudaMemsetAsync(out->fp4_g, 0, sizeof(float), st) != cudaSuccess) return check_launch("dmpq_pack_weights(memset)");
-    const long long nvec = (long long)n * k / 8;
-    int grid = num_sms() * 4;
-    if ((long long)grid * 256 > nvec) grid = (int)((nvec + 255) / 256);
-    amax_bf16_kernel<<<grid, 256, 0, st>>>(W, nvec, out->fp4_g);
-    dmpq_status rc = check_launch("dmpq_pack_weights(amax)");
-    if (rc != DMPQ_OK) return rc;
-    rc = dmpq_global_scale(out->fp4_g, 2688.0f, out->fp4_g, 1, s);
-    if (rc != DMPQ_OK) return rc;
+    dmpq_status rc;
     dmpq_act a{};
     a.fmt = DMPQ_FMT_NVFP4; a.m = n; a.k = k; a.codes = out->fp4_codes; a.sf = out->fp4_sf; a.g = out->fp4_g;
-    rc = dmpq_quantize_act(W, n, k, k, nullptr, nullptr, &a, nullptr, s);
+    dmpq_quant_opts had_opts{};
+    had_opts.flags = DMPQ_QF_HADAMARD;
+    if (had) {
+        // pass 1: amax of the rotated weights (codes are overwritten by pass 2), with g = 1 in i8_scale[0]
+        float* one = out->i8_scale;
+        const float h_one = 1.0f;
+        if (cudaMemcpyAsync(one, &h_one, sizeof(float), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return check_launch("dmpq_pack_weights(memcpy)");
+        dmpq_act probe = a;
+        probe.g = one;
+        rc = dmpq_quantize_act(W, n, k, k, &had_opts, nullptr, &probe, out->fp4_g, s);
+        if (rc != DMPQ_OK) return rc;
+    } else {
+        const long long nvec = (long long)n * k / 8;
+        int grid = num_sms() * 4;
+        if ((long long)grid * 256 > nvec) grid = (int)((nvec + 255) / 256);
+        amax_bf16_kernel<<<grid, 256, 0, st>>>(W, nvec, out->fp4_g);
+        rc = check_launch("dmpq_pack_weights(amax)");
+        if (rc != DMPQ_OK) return rc;
+    }
+    rc = dmpq_global_scale(out->fp4_g, 2688.0f, out->fp4_g, 1, s);
+    if (rc != DMPQ_OK) return rc;
+    rc = dmpq_quantize_act(W, n, k, k, had ? &had_opts : nullptr, nullptr, &a, nullptr, s);
     if (rc != DMPQ_OK) return rc;
     pack_int8_from_fp4_kernel<<<n, 256, 0, st>>>(out->fp4_codes, out->fp4_sf, out->fp4_g, n, k, ((k / 16) + 3) / 4,
                                                  out->i8_codes, out->i8_scale);

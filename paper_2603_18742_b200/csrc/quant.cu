@@ -238,6 +238,180 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Hadamard-smoothed variant (R14): every 128-element block of the (LN'd) row is rotated
+// by the normalized Sylvester FHT before quantization. A block spans 16 consecutive lanes x 8
+// elements: stages h = 1, 2, 4 are in-thread, h = 8..64 exchange with lane ^ (h/8); the fixed
+// stage order and operand order reproduce the oracle's FP32 butterflies bit for bit.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void fht128_vec(float (&y)[8], int lane) {
+#pragma unroll
+    for (int h = 1; h < 8; h <<= 1) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if ((e & h) == 0) {
+                const float a = y[e], b = y[e + h];
+                y[e] = __fadd_rn(a, b);
+                y[e + h] = __fsub_rn(a, b);
+            }
+    }
+#pragma unroll
+    for (int s = 1; s < 16; s <<= 1) {            // element stride h = 8*s
+        const bool upper = (lane & s) != 0;         // this lane holds the (i + h) elements
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float o = __shfl_xor_sync(0xffffffffu, y[e], s);
+            y[e] = upper ? __fsub_rn(o, y[e]) : __fadd_rn(y[e], o);
+        }
+    }
+    const float sc = 0.08838834764831845f;          // fl32(1/sqrt(128))
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = __fmul_rn(y[e], sc);
+}
+
+template <int NV, bool WARP_ROW>
+__global__ void __launch_bounds__(256) quant_act_had_kernel(const QuantParams p) {
+    __shared__ float red[40];
+    RowReduce<WARP_ROW> rr{red};
+    const int lane = threadIdx.x & 31;
+    const int tpr = WARP_ROW ? 32 : blockDim.x;
+    const int tid = WARP_ROW ? lane : threadIdx.x;
+    const int rows_per_cta = WARP_ROW ? (blockDim.x >> 5) : 1;
+    const int row_slot = WARP_ROW ? (threadIdx.x >> 5) : 0;
+    const int nvec = p.k >> 3;
+    const bool want_fp4 = p.fp4_codes != nullptr;
+    const bool want_i8 = p.i8_codes != nullptr;
+    const float g = want_fp4 ? *p.g : 1.0f;
+    const int stride = gridDim.x * rows_per_cta;
+    float cta_amax = 0.0f;
+
+    int row = blockIdx.x * rows_per_cta + row_slot;
+    uint4 v[NV];
+    load_row<NV>(v, p.X + (size_t)row * p.ldx, tid, tpr, nvec, row < p.m);
+    while (row < p.m) {
+        const int next = row + stride;
+        uint4 nv[NV];
+        load_row<NV>(nv, p.X + (size_t)next * p.ldx, tid, tpr, nvec, next < p.m);
+        if (p.flags & DMPQ_QF_LAYERNORM) {
+            f2 s2 = f2make(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                s2 = add2(s2, add2(bf16x2_to_f2(v[i].x), bf16x2_to_f2(v[i].y)));
+                s2 = add2(s2, add2(bf16x2_to_f2(v[i].z), bf16x2_to_f2(v[i].w)));
+            }
+            const float mean = __fdiv_rn(rr.sum(__fadd_rn(f2lo(s2), f2hi(s2))), (float)p.k);
+            f2 q2 = f2make(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                if (tid + i * tpr >= nvec) continue;
+                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const f2 d = add2(bf16x2_to_f2(w[j]), f2make(-mean, -mean));
+                    q2 = add2(q2, mul2(d, d));
+                }
+            }
+            const float var = __fdiv_rn(rr.sum(__fadd_rn(f2lo(q2), f2hi(q2))), (float)p.k);
+            const f2 rstd2 = f2make(__frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps))), 0.0f);
+            const f2 rs = f2make(f2lo(rstd2), f2lo(rstd2));
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) w[j] = pack_bf16x2_f2(mul2(add2(bf16x2_to_f2(w[j]), f2make(-mean, -mean)), rs));
+                v[i] = (vi < nvec) ? make_uint4(w[0], w[1], w[2], w[3]) : make_uint4(0, 0, 0, 0);
+                if ((p.flags & DMPQ_QF_WRITE_H) && vi < nvec)
+                    *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)vi * 8) = v[i];
+            }
+        }
+        float y[NV][8];
+        float vmax[NV];
+        float tmax = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { y[i][2 * j] = bf16lo(w[j]); y[i][2 * j + 1] = bf16hi(w[j]); }
+            fht128_vec(y[i], lane);
+            float mx = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) mx = fmaxf(mx, fabsf(y[i][e]));
+            vmax[i] = (tid + i * tpr < nvec) ? mx : 0.0f;
+            tmax = fmaxf(tmax, vmax[i]);
+        }
+        cta_amax = fmaxf(cta_amax, tmax);
+        if (want_fp4) {
+            uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                const float a_b = fmaxf(vmax[i], __shfl_xor_sync(0xffffffffu, vmax[i], 1));
+                const float raw = __fdiv_rn(__fdiv_rn(a_b, 6.0f), g);
+                const uint32_t sb = e4m3_rn_satfinite(raw);
+                const float eff = __fmul_rn(e4m3_decode(sb), g);
+                const float rcp = eff > 0.0f ? __frcp_rn(eff) : 0.0f;
+                const f2 rcp2 = f2make(rcp, rcp);
+                uint32_t codes = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const f2 q = mul2(f2make(y[i][2 * j], y[i][2 * j + 1]), rcp2);
+                    codes |= e2m1x2(f2lo(q), f2hi(q)) << (8 * j);
+                }
+                const int base = lane & ~7;
+                const uint32_t s0 = __shfl_sync(0xffffffffu, sb, base + 0);
+                const uint32_t s1 = __shfl_sync(0xffffffffu, sb, base + 2);
+                const uint32_t s2 = __shfl_sync(0xffffffffu, sb, base + 4);
+                const uint32_t s3 = __shfl_sync(0xffffffffu, sb, base + 6);
+                if (vi < nvec) {
+                    *reinterpret_cast<uint32_t*>(p.fp4_codes + (size_t)row * (p.k >> 1) + (size_t)vi * 4) = codes;
+                    if ((lane & 7) == 0)
+                        *reinterpret_cast<uint32_t*>(sf_row + (size_t)(vi >> 3) * 512) = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+                }
+            }
+        }
+        if (want_i8) {
+            const float a = rr.max(tmax);
+            const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
+            if (tid == 0) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+            const f2 rcp2 = f2make(rcp, rcp);
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int vi = tid + i * tpr;
+                uint32_t out[2];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const f2 q0 = mul2(f2make(y[i][4 * hh], y[i][4 * hh + 1]), rcp2);
+                    const f2 q1 = mul2(f2make(y[i][4 * hh + 2], y[i][4 * hh + 3]), rcp2);
+                    uint32_t r;
+                    asm("{ .reg .s32 i0, i1, i2, i3; .reg .b32 pp;\n\t"
+                        "cvt.rni.s32.f32 i0, %1; cvt.rni.s32.f32 i1, %2; cvt.rni.s32.f32 i2, %3; cvt.rni.s32.f32 i3, %4;\n\t"
+                        "cvt.pack.sat.s8.s32.b32 pp, i3, i2, 0; cvt.pack.sat.s8.s32.b32 %0, i1, i0, pp; }"
+                        : "=r"(r) : "f"(f2lo(q0)), "f"(f2hi(q0)), "f"(f2lo(q1)), "f"(f2hi(q1)));
+                    out[hh] = r;
+                }
+                if (vi < nvec) *reinterpret_cast<uint2*>(p.i8_codes + (size_t)row * p.k + (size_t)vi * 8) = make_uint2(out[0], out[1]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = nv[i];
+        row = next;
+    }
+    if (want_fp4) {
+        const int pad_rows = p.m_pad - p.m;
+        const int words_per_row = p.kc4;
+        for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < pad_rows * words_per_row; idx += gridDim.x * blockDim.x) {
+            const int r = p.m + idx / words_per_row, c4 = idx % words_per_row;
+            uint8_t* sf_row = p.fp4_sf + (size_t)(r >> 7) * p.kc4 * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4;
+            *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = 0u;
+        }
+    }
+    if (p.amax_out) {
+        float am = warp_max(cta_amax);
+        if (lane == 0) atomic_max_nonneg(p.amax_out, am);
+    }
+}
+
 __global__ void global_scale_kernel(const float* amax, float div, float* g_out, int count) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) {
@@ -253,7 +427,8 @@ static void launch_quant(const QuantParams& p, int threads, cudaStream_t s) {
     int grid = num_sms() * (WR ? 8 : (2048 / threads));
     if (grid > ctas_needed) grid = ctas_needed;
     if (grid < 1) grid = 1;
-    quant_act_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
+    if (p.flags & DMPQ_QF_HADAMARD) quant_act_had_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
+    else quant_act_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
 }
 
 }  // namespace dmpq
@@ -282,6 +457,8 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
     QuantParams p{};
     p.X = X; p.m = m; p.k = k; p.ldx = ldx;
     p.flags = opts ? opts->flags : 0u;
+    DMPQ_REQUIRE(!(p.flags & DMPQ_QF_HADAMARD) || k % 128 == 0, DMPQ_ESHAPE,
+                 "dmpq_quantize_act: DMPQ_QF_HADAMARD needs k %% 128 == 0 (k=%d)", k);
     p.ln_eps = opts ? opts->ln_eps : 0.0f;
     if (p.flags & DMPQ_QF_WRITE_H) {
         DMPQ_REQUIRE(opts->h_out && aligned16(opts->h_out) && opts->ldh >= k && opts->ldh % 8 == 0, DMPQ_EALIGN,

@@ -59,6 +59,7 @@ class PackedWeights:
     i8_scale: torch.Tensor
     bias: torch.Tensor | None
     c: L.Weights = field(default=None, repr=False)
+    hadamard: bool = False
 
     @classmethod
     def empty(cls, n: int, k: int, device, bias: torch.Tensor | None = None):
@@ -80,13 +81,19 @@ class PackedWeights:
                    (self.fp4_codes, self.fp4_sf, self.fp4_g, self.i8_codes, self.i8_scale))
 
 
-def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None) -> PackedWeights:
-    """Offline pack of nn.Linear weights W [n, k] (bf16, CUDA) in both formats (R7)."""
+def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamard: bool = False) -> PackedWeights:
+    """Offline pack of nn.Linear weights W [n, k] (bf16, CUDA) in both formats (P:184, R7);
+    hadamard=True rotates every row by the block FHT first (R14)."""
     _check_dev(W, "W", torch.bfloat16)
     W = W.contiguous()
     n, k = W.shape
     pw = PackedWeights.empty(n, k, W.device, bias)
-    L.check("dmpq_pack_weights", L.lib().dmpq_pack_weights(_ptr(W), n, k, ctypes.byref(pw.c), _stream(W.device)))
+    if hadamard:
+        L.check("dmpq_pack_weights_ex", L.lib().dmpq_pack_weights_ex(_ptr(W), n, k, L.PACK_HADAMARD, ctypes.byref(pw.c),
+                                                                     _stream(W.device)))
+    else:
+        L.check("dmpq_pack_weights", L.lib().dmpq_pack_weights(_ptr(W), n, k, ctypes.byref(pw.c), _stream(W.device)))
+    pw.hadamard = hadamard
     return pw
 
 
@@ -121,14 +128,15 @@ class QuantAct:
 
 def dmpq_quantize_act(X: torch.Tensor, out_i8: QuantAct | None = None, out_fp4: QuantAct | None = None,
                       amax_out: torch.Tensor | None = None, layernorm: bool = False, ln_eps: float = 1e-6,
-                      h_out: torch.Tensor | None = None):
+                      h_out: torch.Tensor | None = None, hadamard: bool = False):
     """Quantize X [m, k] (bf16, CUDA, row stride X.stride(0)) into the given outputs (Eq. 2 / P:115)."""
     _check_dev(X, "X", torch.bfloat16)
     if X.stride(1) != 1:
         raise ValueError("X rows must be contiguous")
     m, k = X.shape
     opts = None
-    flags = (L.QF_LAYERNORM if layernorm else 0) | (L.QF_WRITE_H if h_out is not None else 0)
+    flags = (L.QF_LAYERNORM if layernorm else 0) | (L.QF_WRITE_H if h_out is not None else 0) | \
+        (L.QF_HADAMARD if hadamard else 0)
     if flags:
         opts = L.QuantOpts(flags, ln_eps, None if h_out is None else h_out.data_ptr(),
                            0 if h_out is None else h_out.stride(0))

@@ -60,7 +60,7 @@ def bench_gemm(m, n, k, fmt, nbuf=2):
                 tflops=flops / t / 1e12, frac=flops / t / 1e12 / peak)
 
 
-def bench_quant(m, k, fmt):
+def bench_quant(m, k, fmt, hadamard=False):
     xs = [synth.dit_activation(m, k, seed=i).cuda() for i in range(2)]
     g = torch.tensor([1e-3], device="cuda")
     a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == D.FMT_NVFP4 else None)
@@ -71,13 +71,14 @@ def bench_quant(m, k, fmt):
         x = xs[it[0] % 2]
         it[0] += 1
         if fmt == D.FMT_NVFP4:
-            D.dmpq_quantize_act(x, out_fp4=a, amax_out=amax)
+            D.dmpq_quantize_act(x, out_fp4=a, amax_out=amax, hadamard=hadamard)
         else:
-            D.dmpq_quantize_act(x, out_i8=a, amax_out=amax)
+            D.dmpq_quantize_act(x, out_i8=a, amax_out=amax, hadamard=hadamard)
     t = timeit(run)
     bpe = 2 + 0.5 + 1 / 16 if fmt == D.FMT_NVFP4 else 2 + 1 + 4 / k
     gbs = m * k * bpe / t / 1e9
-    return dict(kernel="quant_" + ("nvfp4" if fmt == D.FMT_NVFP4 else "int8"), m=m, k=k, us=t * 1e6, gbs=gbs,
+    return dict(kernel="quant_" + ("nvfp4" if fmt == D.FMT_NVFP4 else "int8") + ("_had" if hadamard else ""), m=m, k=k,
+                us=t * 1e6, gbs=gbs,
                 frac=gbs / PEAKS["hbm_gbs"])
 
 
@@ -125,9 +126,10 @@ def main():
     if a.quant:
         for (m, k) in [(35552, 3072), (35552, 12288), (65536, 1920)]:
             for fmt in (D.FMT_NVFP4, D.FMT_INT8):
-                r = bench_quant(m, k, fmt)
-                print(json.dumps(r), flush=True)
-                res.append(r)
+                for had in (False, True):
+                    r = bench_quant(m, k, fmt, had)
+                    print(json.dumps(r), flush=True)
+                    res.append(r)
     if a.tdc:
         for r in bench_tdc(35552, 3072):
             print(json.dumps(r), flush=True)

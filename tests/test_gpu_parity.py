@@ -199,3 +199,60 @@ def test_tdc_refresh_and_skip(D, orc, m, h):
     D.tdc_step(0, x, x, delta)
     torch.cuda.synchronize()
     assert np.array_equal(synth.bits(x.cpu()), orc.tdc_skip(_u16(xi), dn_ref))
+
+
+@pytest.mark.parametrize("m,k,ln", [(5, 128, False), (130, 3072, True), (37, 1920, False), (33, 12288, False)])
+def test_quantize_hadamard_bit_exact(D, orc, m, k, ln):
+    """Online block Hadamard fused into the quantizer (R14): codes and scales
+    equal the oracle's FP32 FHT followed by the FP32-input quantizers."""
+    x = synth.dit_activation(m, k, seed=m + 3 * k)
+    h = torch.empty(m, k, dtype=torch.bfloat16, device="cuda") if ln else None
+    g = torch.tensor([0.01], device="cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    amax = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a8, out_fp4=a4, amax_out=amax, layernorm=ln, h_out=h, hadamard=True)
+    torch.cuda.synchronize()
+    src = synth.bits(h.cpu()) if ln else synth.bits(x)
+    y = orc.fht128(orc.bf16_to_f32(src).reshape(m, k))
+    assert amax.item() == float(np.abs(y).max())
+    c4, s4 = orc.nvfp4_quantize_f32(y, 0.01)
+    assert np.array_equal(a4.codes.cpu().numpy(), c4)
+    assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s4)
+    c8, s8 = orc.int8_quantize_f32(y)
+    assert np.array_equal(a8.codes.cpu().numpy(), c8)
+    assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+
+
+@pytest.mark.parametrize("n,k", [(128, 128), (256, 1920)])
+def test_pack_weights_hadamard_and_gemm(D, orc, n, k):
+    """Rotated weights pack bit-exact; the rotated GEMM reproduces the unrotated layer
+    (H orthogonal: (Hx).(Hw) = x.w) up to quantization."""
+    w, b = synth.linear_weight(n, k, seed=n + 7 * k)
+    pw = D.dmpq_pack_weights(w.cuda(), b, hadamard=True)
+    torch.cuda.synchronize()
+    ref = orc.pack_weights_hadamard(synth.bits(w))
+    assert pw.fp4_g.item() == ref["fp4_g"]
+    assert np.array_equal(pw.fp4_codes.cpu().numpy(), ref["fp4_codes"])
+    assert np.array_equal(orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k), ref["fp4_sf"])
+    assert np.array_equal(pw.i8_codes.cpu().numpy(), ref["i8_codes"])
+    assert np.array_equal(pw.i8_scale.cpu().numpy(), ref["i8_scale"])
+    m = 96
+    x = synth.dit_activation(m, k, seed=5)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a8, hadamard=True)
+    y = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a8, pw, Y32=y)
+    torch.cuda.synchronize()
+    exact = x.float().numpy().astype(np.float64) @ w.float().numpy().astype(np.float64).T + b.numpy()
+    # the unrotated quantized layer on the same input, for comparison
+    pw0 = D.dmpq_pack_weights(w.cuda(), b)
+    a0 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a0)
+    y0 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a0, pw0, Y32=y0)
+    torch.cuda.synchronize()
+    err_rot = np.linalg.norm(y.cpu().numpy() - exact) / np.linalg.norm(exact)
+    err_plain = np.linalg.norm(y0.cpu().numpy() - exact) / np.linalg.norm(exact)
+    # transparent up to quantization (4-bit-derived weights): same error scale as the plain path
+    assert err_rot < 0.25 and err_rot < 1.5 * err_plain, (err_rot, err_plain)
