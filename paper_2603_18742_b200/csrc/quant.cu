@@ -2,13 +2,10 @@
 // quantization (Eq. 2; R2-R6), optionally
 // with a fused row LayerNorm prologue (block glue), and dmpq_global_scale.
 //
-// HBM-bound streaming kernel. Each row is held in registers by one warp (k <= 512)
-// or one CTA (k > 512): NV 16-byte vectors (8 bf16) per thread, loaded once,
-// coalesced (consecutive lanes own consecutive vectors). Reductions: warp
-// shuffles + shared memory, fixed order (deterministic). Per 16-element NVFP4
-// block the two lanes holding it exchange their maxima with one shuffle; four
-// consecutive blocks' E4M3 scales (one 32-bit word of the swizzled scale layout)
-// are gathered by shuffles and stored by one lane. Persistent grid over rows.
+// HBM-bound streaming kernel: each row is held in registers by a group of threads
+// (64-element chunks per thread, one 128-byte line each), the next row prefetched
+// while the current one is processed; fixed-order reductions (deterministic);
+// persistent grid over rows.
 #include <cstdio>
 
 #include "common.cuh"
@@ -31,6 +28,318 @@ struct QuantParams {
     int kc4;     // scale-column atoms per 128-row tile: ceil(k/16/4)
     int m_pad;   // rows rounded up to 128 (scale rows to zero-fill)
 };
+
+// ---------------------------------------------------------------------------------------------
+// Hadamard path (R14). Layout: a row is quantised by a group of `tpr` threads (a multiple of 32); each thread owns
+// chunks of 64 consecutive elements (8 x 16-byte loads, one full 128-byte line), chunk
+// c = tid + i*tpr. A chunk holds four whole NVFP4 blocks and exactly one 32-bit word of the
+// scale-atom layout (c == atom column), so block maxima and the scale store need no lane
+// exchange; with the Hadamard option, FHT stages h = 1..32 are in-thread and h = 64 pairs
+// lanes (tid ^ 1). Group reductions: warp shuffles, then smem + a named barrier per group.
+// ---------------------------------------------------------------------------------------------
+struct GroupReduce {
+    float* red;      // [6 areas][8 groups][8 warps]
+    int tpr, group, warp_in_group, lane;
+    __device__ __forceinline__ float sum(float v, int area) {
+        v = warp_sum(v);
+        if (tpr == 32) return v;
+        float* r = red + (area * 8 + group) * 8;
+        if (lane == 0) r[warp_in_group] = v;
+        named_barrier(1 + group, tpr);
+        float t = 0.0f;
+        for (int w = 0; w < (tpr >> 5); ++w) t = __fadd_rn(t, r[w]);
+        return t;
+    }
+    __device__ __forceinline__ float max(float v, int area) {
+        v = warp_max(v);
+        if (tpr == 32) return v;
+        float* r = red + (area * 8 + group) * 8;
+        if (lane == 0) r[warp_in_group] = v;
+        named_barrier(1 + group, tpr);
+        float t = 0.0f;
+        for (int w = 0; w < (tpr >> 5); ++w) t = fmaxf(t, r[w]);
+        return t;
+    }
+    __device__ __forceinline__ static void named_barrier(int id, int n) {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    }
+};
+
+// bf16 pair (one 32-bit word) -> packed fp32x2 (exact widening)
+__device__ __forceinline__ f2 bf16x2_to_f2(uint32_t w) { return f2make(bf16lo(w), bf16hi(w)); }
+
+// |x| max over 8 packed bf16 words (16 elements), in the bf16 domain (exact)
+__device__ __forceinline__ float absmax16(const uint32_t* w) {
+    uint32_t m;
+    asm("{ .reg .b32 a0, a1, a2, a3, a4, a5, a6, a7, t0, t1, t2, t3, u0, u1;\n\t"
+        "and.b32 a0, %1, 0x7fff7fff; and.b32 a1, %2, 0x7fff7fff; and.b32 a2, %3, 0x7fff7fff; and.b32 a3, %4, 0x7fff7fff;\n\t"
+        "and.b32 a4, %5, 0x7fff7fff; and.b32 a5, %6, 0x7fff7fff; and.b32 a6, %7, 0x7fff7fff; and.b32 a7, %8, 0x7fff7fff;\n\t"
+        "max.bf16x2 t0, a0, a1; max.bf16x2 t1, a2, a3; max.bf16x2 t2, a4, a5; max.bf16x2 t3, a6, a7;\n\t"
+        "max.bf16x2 u0, t0, t1; max.bf16x2 u1, t2, t3; max.bf16x2 %0, u0, u1; }"
+        : "=r"(m) : "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]));
+    return fmaxf(bf16lo(m), bf16hi(m));
+}
+
+// NVFP4 block scale of Eq. 2 with the two-level scale (R3/R4): returns the E4M3 code, sets rcp = fl(1/eff)
+__device__ __forceinline__ uint32_t nvfp4_block_scale(float a_b, float g, float& rcp) {
+    const float raw = __fdiv_rn(__fdiv_rn(a_b, 6.0f), g);
+    const uint32_t sb = e4m3_rn_satfinite(raw);
+    const float eff = __fmul_rn(e4m3_decode(sb), g);
+    rcp = eff > 0.0f ? __frcp_rn(eff) : 0.0f;
+    return sb;
+}
+
+// four int8 codes RNE(q * rcp) (saturating pack; the clamp never binds). Byte order q0..q3.
+__device__ __forceinline__ uint32_t int8x4(f2 q01, f2 q23) {
+    uint32_t r;
+    asm("{ .reg .s32 i0, i1, i2, i3; .reg .b32 pp;\n\t"
+        "cvt.rni.s32.f32 i0, %1; cvt.rni.s32.f32 i1, %2; cvt.rni.s32.f32 i2, %3; cvt.rni.s32.f32 i3, %4;\n\t"
+        "cvt.pack.sat.s8.s32.b32 pp, i3, i2, 0; cvt.pack.sat.s8.s32.b32 %0, i1, i0, pp; }"
+        : "=r"(r) : "f"(f2lo(q01)), "f"(f2hi(q01)), "f"(f2lo(q23)), "f"(f2hi(q23)));
+    return r;
+}
+
+// FHT over the 128-element block held by this thread (64 elements) and its partner lane
+// (tid ^ 1): stages h = 1..32 in-thread (packed), h = 64 across the pair, then * fl32(1/sqrt(128)).
+// Every butterfly is one FP32 add/sub in the oracle's order (bit-exact, R14).
+__device__ __forceinline__ void fht128_chunk(float (&y)[64], bool upper) {
+    // h = 1: pairs (e, e+1), e even; pack two pairs per instruction
+#pragma unroll
+    for (int e = 0; e < 64; e += 4) {
+        const f2 a = f2make(y[e], y[e + 2]), b = f2make(y[e + 1], y[e + 3]);
+        const f2 s = add2(a, b), d = add2(a, f2make(-y[e + 1], -y[e + 3]));
+        y[e] = f2lo(s); y[e + 2] = f2hi(s); y[e + 1] = f2lo(d); y[e + 3] = f2hi(d);
+    }
+#pragma unroll
+    for (int h = 2; h < 64; h <<= 1) {
+#pragma unroll
+        for (int e = 0; e < 64; e += 2) {
+            if (e & h) continue;
+            const f2 a = f2make(y[e], y[e + 1]), b = f2make(y[e + h], y[e + h + 1]);
+            const f2 s = add2(a, b), d = add2(a, f2make(-y[e + h], -y[e + h + 1]));
+            y[e] = f2lo(s); y[e + 1] = f2hi(s); y[e + h] = f2lo(d); y[e + h + 1] = f2hi(d);
+        }
+    }
+    // h = 64: lower lane keeps a + b, upper lane gets a - b = fma(-1, b, a) (exact product, one rounding)
+    const f2 sg = upper ? f2make(-1.0f, -1.0f) : f2make(1.0f, 1.0f);
+#pragma unroll
+    for (int e = 0; e < 64; e += 2) {
+        const float o0 = __shfl_xor_sync(0xffffffffu, y[e], 1), o1 = __shfl_xor_sync(0xffffffffu, y[e + 1], 1);
+        const f2 r = fma2(sg, f2make(y[e], y[e + 1]), f2make(o0, o1));
+        y[e] = f2lo(r); y[e + 1] = f2hi(r);
+    }
+    const f2 sc = f2make(0.08838834764831845f, 0.08838834764831845f);   // fl32(1/sqrt(128))
+#pragma unroll
+    for (int e = 0; e < 64; e += 2) {
+        const f2 r = mul2(f2make(y[e], y[e + 1]), sc);
+        y[e] = f2lo(r); y[e + 1] = f2hi(r);
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ void load_chunks(uint4 (&v)[NC][8], const uint16_t* xr, int tid, int tpr, int nch, bool valid) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+        const int c = tid + i * tpr;
+        const bool ok = valid && c < nch;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            v[i][j] = ok ? *reinterpret_cast<const uint4*>(xr + (size_t)c * 64 + j * 8) : make_uint4(0, 0, 0, 0);
+    }
+}
+
+template <int NC, bool HAD>
+__global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams p, int tpr) {
+    __shared__ float red[6 * 8 * 8];
+    const int lane = threadIdx.x & 31;
+    const int group = threadIdx.x / tpr, tid = threadIdx.x % tpr;
+    const int groups = blockDim.x / tpr;
+    GroupReduce gr{red, tpr, group, tid >> 5, lane};
+    const int nch = p.k >> 6;
+    const bool want_fp4 = p.fp4_codes != nullptr;
+    const bool want_i8 = p.i8_codes != nullptr;
+    const float g = want_fp4 ? *p.g : 1.0f;
+    const int stride = gridDim.x * groups;
+    float my_amax = 0.0f;
+    int parity = 0;
+
+    int row = blockIdx.x * groups + group;
+    uint4 v[NC][8];
+    load_chunks<NC>(v, p.X + (size_t)row * p.ldx, tid, tpr, nch, row < p.m);
+    while (row < p.m) {
+        const int next = row + stride;
+        uint4 nv[NC][8];   // prefetch the next row while this one is processed
+        load_chunks<NC>(nv, p.X + (size_t)next * p.ldx, tid, tpr, nch, next < p.m);
+        const int a0 = parity * 3;
+        if (p.flags & DMPQ_QF_LAYERNORM) {
+            // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue, R13)
+            f2 s2 = f2make(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    s2 = add2(s2, add2(bf16x2_to_f2(v[i][j].x), bf16x2_to_f2(v[i][j].y)));
+                    s2 = add2(s2, add2(bf16x2_to_f2(v[i][j].z), bf16x2_to_f2(v[i][j].w)));
+                }
+            const float mean = __fdiv_rn(gr.sum(__fadd_rn(f2lo(s2), f2hi(s2)), a0 + 0), (float)p.k);
+            const f2 nm = f2make(-mean, -mean);
+            f2 q2 = f2make(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                if (tid + i * tpr >= nch) continue;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t w[4] = {v[i][j].x, v[i][j].y, v[i][j].z, v[i][j].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const f2 d = add2(bf16x2_to_f2(w[t]), nm);
+                        q2 = add2(q2, mul2(d, d));
+                    }
+                }
+            }
+            const float var = __fdiv_rn(gr.sum(__fadd_rn(f2lo(q2), f2hi(q2)), a0 + 1), (float)p.k);
+            const float rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps)));
+            const f2 rs = f2make(rstd, rstd);
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const int c = tid + i * tpr;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t w[4] = {v[i][j].x, v[i][j].y, v[i][j].z, v[i][j].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) w[t] = pack_bf16x2_f2(mul2(add2(bf16x2_to_f2(w[t]), nm), rs));
+                    v[i][j] = (c < nch) ? make_uint4(w[0], w[1], w[2], w[3]) : make_uint4(0, 0, 0, 0);
+                    if ((p.flags & DMPQ_QF_WRITE_H) && c < nch)
+                        *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)c * 64 + j * 8) = v[i][j];
+                }
+            }
+        }
+        // per-16-block |x| maxima (4 per chunk) and this thread's row maximum
+        float bmax[NC][4];
+        float tmax = 0.0f;
+        float y[HAD ? NC : 1][HAD ? 64 : 1];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+            const bool ok = tid + i * tpr < nch;
+            if constexpr (HAD) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t w[4] = {v[i][j].x, v[i][j].y, v[i][j].z, v[i][j].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) { y[i][8 * j + 2 * t] = bf16lo(w[t]); y[i][8 * j + 2 * t + 1] = bf16hi(w[t]); }
+                }
+                fht128_chunk(y[i], (tid & 1) != 0);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    float mx = 0.0f;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(y[i][16 * b + e]));
+                    bmax[i][b] = ok ? mx : 0.0f;
+                }
+            } else {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t w[8] = {v[i][2 * b].x, v[i][2 * b].y, v[i][2 * b].z, v[i][2 * b].w,
+                                           v[i][2 * b + 1].x, v[i][2 * b + 1].y, v[i][2 * b + 1].z, v[i][2 * b + 1].w};
+                    bmax[i][b] = absmax16(w);
+                }
+            }
+            tmax = fmaxf(tmax, fmaxf(fmaxf(bmax[i][0], bmax[i][1]), fmaxf(bmax[i][2], bmax[i][3])));
+        }
+        my_amax = fmaxf(my_amax, tmax);
+
+        if (want_fp4) {
+            uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const int c = tid + i * tpr;
+                if (c >= nch) continue;
+                uint32_t sfw = 0;
+                uint32_t codes[8];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    float rcp;
+                    sfw |= nvfp4_block_scale(bmax[i][b], g, rcp) << (8 * b);
+                    const f2 r2 = f2make(rcp, rcp);
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {   // 8 elements -> one 32-bit word of codes
+                        uint32_t cw = 0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int e = 16 * b + 8 * t + 2 * u;
+                            f2 q;
+                            if constexpr (HAD) q = mul2(f2make(y[i][e], y[i][e + 1]), r2);
+                            else {
+                                const uint4& vv = v[i][e >> 3];
+                                const uint32_t ww = ((e & 7) == 0) ? vv.x : ((e & 7) == 2) ? vv.y : ((e & 7) == 4) ? vv.z : vv.w;
+                                q = mul2(bf16x2_to_f2(ww), r2);
+                            }
+                            cw |= e2m1x2(f2lo(q), f2hi(q)) << (8 * u);
+                        }
+                        codes[2 * b + t] = cw;
+                    }
+                }
+                uint4* cp = reinterpret_cast<uint4*>(p.fp4_codes + (size_t)row * (p.k >> 1) + (size_t)c * 32);
+                cp[0] = make_uint4(codes[0], codes[1], codes[2], codes[3]);
+                cp[1] = make_uint4(codes[4], codes[5], codes[6], codes[7]);
+                *reinterpret_cast<uint32_t*>(sf_row + (size_t)c * 512) = sfw;
+            }
+        }
+        if (want_i8) {
+            const float a = gr.max(tmax, a0 + 2);
+            const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
+            if (tid == 0) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+            const f2 r2 = f2make(rcp, rcp);
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const int c = tid + i * tpr;
+                if (c >= nch) continue;
+                uint4* op = reinterpret_cast<uint4*>(p.i8_codes + (size_t)row * p.k + (size_t)c * 64);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {   // 16 elements -> one 16-byte store
+                    uint32_t o[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int e = 16 * j + 4 * t;
+                        f2 q0, q1;
+                        if constexpr (HAD) {
+                            q0 = mul2(f2make(y[i][e], y[i][e + 1]), r2);
+                            q1 = mul2(f2make(y[i][e + 2], y[i][e + 3]), r2);
+                        } else {
+                            const uint4& vv = v[i][e >> 3];
+                            const uint32_t w0 = ((e & 7) == 0) ? vv.x : vv.z, w1 = ((e & 7) == 0) ? vv.y : vv.w;
+                            q0 = mul2(bf16x2_to_f2(w0), r2);
+                            q1 = mul2(bf16x2_to_f2(w1), r2);
+                        }
+                        o[t] = int8x4(q0, q1);
+                    }
+                    op[j] = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NC; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[i][j] = nv[i][j];
+        row = next;
+        parity ^= 1;
+    }
+    // zero the scale rows that pad m up to a multiple of 128 (read by the GEMM's M tail)
+    if (want_fp4) {
+        const int pad_rows = p.m_pad - p.m;
+        const int words_per_row = p.kc4;
+        for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < pad_rows * words_per_row; idx += gridDim.x * blockDim.x) {
+            const int r = p.m + idx / words_per_row, c4 = idx % words_per_row;
+            uint8_t* sf_row = p.fp4_sf + (size_t)(r >> 7) * p.kc4 * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4;
+            *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = 0u;
+        }
+    }
+    if (p.amax_out) {
+        const float am = warp_max(my_amax);
+        if (lane == 0) atomic_max_nonneg(p.amax_out, am);
+    }
+}
+
 
 template <bool WARP_ROW>
 struct RowReduce {
@@ -57,8 +366,6 @@ struct RowReduce {
     }
 };
 
-// bf16 pair (one 32-bit word) -> packed fp32x2 (exact widening)
-__device__ __forceinline__ f2 bf16x2_to_f2(uint32_t w) { return f2make(bf16lo(w), bf16hi(w)); }
 
 // |x| max over a vector of 8 bf16, in the bf16 domain (exact): max.bf16x2 on sign-cleared words
 __device__ __forceinline__ float vec_absmax(const uint4& v) {
@@ -238,186 +545,23 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
     }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Hadamard-smoothed variant (R14): every 128-element block of the (LN'd) row is rotated
-// by the normalized Sylvester FHT before quantization. A block spans 16 consecutive lanes x 8
-// elements: stages h = 1, 2, 4 are in-thread, h = 8..64 exchange with lane ^ (h/8); the fixed
-// stage order and operand order reproduce the oracle's FP32 butterflies bit for bit.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void fht128_vec(float (&y)[8], int lane) {
-#pragma unroll
-    for (int h = 1; h < 8; h <<= 1) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if ((e & h) == 0) {
-                const float a = y[e], b = y[e + h];
-                y[e] = __fadd_rn(a, b);
-                y[e + h] = __fsub_rn(a, b);
-            }
-    }
-#pragma unroll
-    for (int s = 1; s < 16; s <<= 1) {            // element stride h = 8*s
-        const bool upper = (lane & s) != 0;         // this lane holds the (i + h) elements
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const float o = __shfl_xor_sync(0xffffffffu, y[e], s);
-            y[e] = upper ? __fsub_rn(o, y[e]) : __fadd_rn(y[e], o);
-        }
-    }
-    const float sc = 0.08838834764831845f;          // fl32(1/sqrt(128))
-#pragma unroll
-    for (int e = 0; e < 8; ++e) y[e] = __fmul_rn(y[e], sc);
-}
-
-template <int NV, bool WARP_ROW>
-__global__ void __launch_bounds__(256) quant_act_had_kernel(const QuantParams p) {
-    __shared__ float red[40];
-    RowReduce<WARP_ROW> rr{red};
-    const int lane = threadIdx.x & 31;
-    const int tpr = WARP_ROW ? 32 : blockDim.x;
-    const int tid = WARP_ROW ? lane : threadIdx.x;
-    const int rows_per_cta = WARP_ROW ? (blockDim.x >> 5) : 1;
-    const int row_slot = WARP_ROW ? (threadIdx.x >> 5) : 0;
-    const int nvec = p.k >> 3;
-    const bool want_fp4 = p.fp4_codes != nullptr;
-    const bool want_i8 = p.i8_codes != nullptr;
-    const float g = want_fp4 ? *p.g : 1.0f;
-    const int stride = gridDim.x * rows_per_cta;
-    float cta_amax = 0.0f;
-
-    int row = blockIdx.x * rows_per_cta + row_slot;
-    uint4 v[NV];
-    load_row<NV>(v, p.X + (size_t)row * p.ldx, tid, tpr, nvec, row < p.m);
-    while (row < p.m) {
-        const int next = row + stride;
-        uint4 nv[NV];
-        load_row<NV>(nv, p.X + (size_t)next * p.ldx, tid, tpr, nvec, next < p.m);
-        if (p.flags & DMPQ_QF_LAYERNORM) {
-            f2 s2 = f2make(0.0f, 0.0f);
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                s2 = add2(s2, add2(bf16x2_to_f2(v[i].x), bf16x2_to_f2(v[i].y)));
-                s2 = add2(s2, add2(bf16x2_to_f2(v[i].z), bf16x2_to_f2(v[i].w)));
-            }
-            const float mean = __fdiv_rn(rr.sum(__fadd_rn(f2lo(s2), f2hi(s2))), (float)p.k);
-            f2 q2 = f2make(0.0f, 0.0f);
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                if (tid + i * tpr >= nvec) continue;
-                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const f2 d = add2(bf16x2_to_f2(w[j]), f2make(-mean, -mean));
-                    q2 = add2(q2, mul2(d, d));
-                }
-            }
-            const float var = __fdiv_rn(rr.sum(__fadd_rn(f2lo(q2), f2hi(q2))), (float)p.k);
-            const f2 rstd2 = f2make(__frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps))), 0.0f);
-            const f2 rs = f2make(f2lo(rstd2), f2lo(rstd2));
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int vi = tid + i * tpr;
-                uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) w[j] = pack_bf16x2_f2(mul2(add2(bf16x2_to_f2(w[j]), f2make(-mean, -mean)), rs));
-                v[i] = (vi < nvec) ? make_uint4(w[0], w[1], w[2], w[3]) : make_uint4(0, 0, 0, 0);
-                if ((p.flags & DMPQ_QF_WRITE_H) && vi < nvec)
-                    *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)vi * 8) = v[i];
-            }
-        }
-        float y[NV][8];
-        float vmax[NV];
-        float tmax = 0.0f;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) { y[i][2 * j] = bf16lo(w[j]); y[i][2 * j + 1] = bf16hi(w[j]); }
-            fht128_vec(y[i], lane);
-            float mx = 0.0f;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) mx = fmaxf(mx, fabsf(y[i][e]));
-            vmax[i] = (tid + i * tpr < nvec) ? mx : 0.0f;
-            tmax = fmaxf(tmax, vmax[i]);
-        }
-        cta_amax = fmaxf(cta_amax, tmax);
-        if (want_fp4) {
-            uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int vi = tid + i * tpr;
-                const float a_b = fmaxf(vmax[i], __shfl_xor_sync(0xffffffffu, vmax[i], 1));
-                const float raw = __fdiv_rn(__fdiv_rn(a_b, 6.0f), g);
-                const uint32_t sb = e4m3_rn_satfinite(raw);
-                const float eff = __fmul_rn(e4m3_decode(sb), g);
-                const float rcp = eff > 0.0f ? __frcp_rn(eff) : 0.0f;
-                const f2 rcp2 = f2make(rcp, rcp);
-                uint32_t codes = 0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const f2 q = mul2(f2make(y[i][2 * j], y[i][2 * j + 1]), rcp2);
-                    codes |= e2m1x2(f2lo(q), f2hi(q)) << (8 * j);
-                }
-                const int base = lane & ~7;
-                const uint32_t s0 = __shfl_sync(0xffffffffu, sb, base + 0);
-                const uint32_t s1 = __shfl_sync(0xffffffffu, sb, base + 2);
-                const uint32_t s2 = __shfl_sync(0xffffffffu, sb, base + 4);
-                const uint32_t s3 = __shfl_sync(0xffffffffu, sb, base + 6);
-                if (vi < nvec) {
-                    *reinterpret_cast<uint32_t*>(p.fp4_codes + (size_t)row * (p.k >> 1) + (size_t)vi * 4) = codes;
-                    if ((lane & 7) == 0)
-                        *reinterpret_cast<uint32_t*>(sf_row + (size_t)(vi >> 3) * 512) = s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
-                }
-            }
-        }
-        if (want_i8) {
-            const float a = rr.max(tmax);
-            const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
-            if (tid == 0) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
-            const f2 rcp2 = f2make(rcp, rcp);
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int vi = tid + i * tpr;
-                uint32_t out[2];
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const f2 q0 = mul2(f2make(y[i][4 * hh], y[i][4 * hh + 1]), rcp2);
-                    const f2 q1 = mul2(f2make(y[i][4 * hh + 2], y[i][4 * hh + 3]), rcp2);
-                    uint32_t r;
-                    asm("{ .reg .s32 i0, i1, i2, i3; .reg .b32 pp;\n\t"
-                        "cvt.rni.s32.f32 i0, %1; cvt.rni.s32.f32 i1, %2; cvt.rni.s32.f32 i2, %3; cvt.rni.s32.f32 i3, %4;\n\t"
-                        "cvt.pack.sat.s8.s32.b32 pp, i3, i2, 0; cvt.pack.sat.s8.s32.b32 %0, i1, i0, pp; }"
-                        : "=r"(r) : "f"(f2lo(q0)), "f"(f2hi(q0)), "f"(f2lo(q1)), "f"(f2hi(q1)));
-                    out[hh] = r;
-                }
-                if (vi < nvec) *reinterpret_cast<uint2*>(p.i8_codes + (size_t)row * p.k + (size_t)vi * 8) = make_uint2(out[0], out[1]);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < NV; ++i) v[i] = nv[i];
-        row = next;
-    }
-    if (want_fp4) {
-        const int pad_rows = p.m_pad - p.m;
-        const int words_per_row = p.kc4;
-        for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < pad_rows * words_per_row; idx += gridDim.x * blockDim.x) {
-            const int r = p.m + idx / words_per_row, c4 = idx % words_per_row;
-            uint8_t* sf_row = p.fp4_sf + (size_t)(r >> 7) * p.kc4 * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4;
-            *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = 0u;
-        }
-    }
-    if (p.amax_out) {
-        float am = warp_max(cta_amax);
-        if (lane == 0) atomic_max_nonneg(p.amax_out, am);
-    }
-}
-
 __global__ void global_scale_kernel(const float* amax, float div, float* g_out, int count) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) {
         float g = __fdiv_rn(amax[i], div);
         g_out[i] = g < 1.17549435e-38f ? 1.17549435e-38f : g;
     }
+}
+
+template <int NC>
+static void launch_quant_had(const QuantParams& p, int tpr, cudaStream_t s) {
+    const int groups = (256 % tpr == 0) ? 256 / tpr : 1;
+    const int threads = groups * tpr;
+    int ctas_needed = (p.m + groups - 1) / groups;
+    int grid = num_sms() * (2048 / threads);
+    if (grid > ctas_needed) grid = ctas_needed;
+    if (grid < 1) grid = 1;
+    quant_act_chunk_kernel<NC, true><<<grid, threads, 0, s>>>(p, tpr);
 }
 
 template <int NV, bool WR>
@@ -427,8 +571,7 @@ static void launch_quant(const QuantParams& p, int threads, cudaStream_t s) {
     int grid = num_sms() * (WR ? 8 : (2048 / threads));
     if (grid > ctas_needed) grid = ctas_needed;
     if (grid < 1) grid = 1;
-    if (p.flags & DMPQ_QF_HADAMARD) quant_act_had_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
-    else quant_act_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
+    quant_act_kernel<NV, WR><<<grid, threads, 0, s>>>(p);
 }
 
 }  // namespace dmpq
@@ -476,6 +619,13 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
     if (m == 0) return DMPQ_OK;
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_quantize_act: needs an sm_100 device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+    if (p.flags & DMPQ_QF_HADAMARD) {
+        // chunk layout: 64 elements per thread, FHT stages 1..32 in-thread
+        const int nch = k / 64;
+        const int tpr = (nch + 31) / 32 * 32;
+        launch_quant_had<1>(p, tpr, st);
+        return check_launch("dmpq_quantize_act");
+    }
     const int nvec = k / 8;
     if (nvec <= 64) {  // warp per row
         if (nvec <= 32) launch_quant<1, true>(p, 256, st);
