@@ -187,7 +187,8 @@ def run_ours(args):
     T = max(T, args.warmup + args.steps)
     peaks, peak_kind = load_peaks()
 
-    model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard)
+    model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
+                     pdr=args.pdr, m_total=M)
     # block-0 input trajectory basis (this rank's rows)
     A, B = synth.trajectory_basis(m, H, seed=1000 + rank, device=dev)
 
@@ -306,7 +307,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (the GEMM format with the most time)
     sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     by_fmt = {}
-    for f, name, ratio in ((D.FMT_NVFP4, "nvfp4", 4), (D.FMT_INT8, "int8", 2)):
+    for f, name, ratio in ((D.FMT_NVFP4, "nvfp4", 4), (D.FMT_INT8, "int8", 2), (D.FMT_BF16, "bf16", 1)):
         secs, n = gemm_t[f]
         if n:
             ach = gemm_flops[f] / secs / 1e12
@@ -322,8 +323,8 @@ def run_ours(args):
         d = by_fmt[dom]
         roofline = {"bound": "tensor", "kernel": f"dmpq_gemm ({dom})", "achieved": d["achieved"], "peak": d["peak"],
                     "unit": "TFLOP/s", "frac": d["frac"], "traffic": traffic,
-                    "peak_source": f"{peak_kind} bf16 sustained {sus} TF/s x {4 if dom == 'nvfp4' else 2} "
-                                   f"(nominal {'fp4' if dom == 'nvfp4' else 'int8'}:bf16 ratio)",
+                    "peak_source": f"{peak_kind} bf16 sustained {sus} TF/s x {dict(nvfp4=4, int8=2, bf16=1)[dom]} "
+                                   f"(nominal {dom}:bf16 ratio)",
                     "by_format": by_fmt}
 
     cpu = None
@@ -339,7 +340,7 @@ def run_ours(args):
         "config": {"workload": desc, "blocks": nb, "hidden": H, "ffn": F, "tokens_total": M, "tokens_per_rank": m,
                    "timesteps": list(range(args.warmup, args.warmup + args.steps)), "T": T,
                    "parallelism": f"token-shard x{world}", "l2": "inputs larger than L2 (multi-GB working set per step)",
-                   "hadamard": not args.no_hadamard,
+                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr,
                    "mix": mix},
         "block_step_ms": elapsed / args.steps / nb * 1e3,
         "effective_tflops_dense_equiv": dense_flops / elapsed / 1e12,
@@ -367,6 +368,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
+    ap.add_argument("--pdr", action="store_true", help="enable the Purified Cache Refresh outlier gate (P:241, "
+                    "NEXT-3; off by default: the north_star path is DMPQ + TDC)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs --warmup >= 3", file=sys.stderr)

@@ -48,8 +48,9 @@ typedef enum {
     DMPQ_EUNSUPPORTED = 6  /* no sm_100a device / feature not built               */
 } dmpq_status;
 
-/* Activation precision of one linear layer, Eq. 7. */
-typedef enum { DMPQ_FMT_INT8 = 0, DMPQ_FMT_NVFP4 = 1 } dmpq_fmt;
+/* Activation precision of one linear layer: Eq. 7 routes INT8 / NVFP4;
+ * the Purified Cache Refresh outlier gate (R15) routes BF16 (unquantised). */
+typedef enum { DMPQ_FMT_INT8 = 0, DMPQ_FMT_NVFP4 = 1, DMPQ_FMT_BF16 = 2 } dmpq_fmt;
 
 const char* dmpq_last_error(void);
 const char* dmpq_version(void);
@@ -87,13 +88,14 @@ typedef struct {
     int8_t* i8_codes;      /* [n x k] */
     float* i8_scale;       /* [n]: per-output-channel scale */
     const float* bias;     /* [n] or NULL (may point at caller memory) */
+    const uint16_t* bf16_w;/* [n x k] original bf16 weights for the BF16 fallback (R15), or NULL */
 } dmpq_weights;
 
 /* A quantized activation tensor, as written by dmpq_quantize_act. */
 typedef struct {
     dmpq_fmt fmt;
     int m, k;
-    void* codes;           /* NVFP4: uint8 [m x k/2]; INT8: int8 [m x k] (row-major, dense) */
+    void* codes;           /* NVFP4: uint8 [m x k/2]; INT8: int8 [m x k]; BF16: the bf16 activation [m x k] (row-major, dense) */
     uint8_t* sf;           /* NVFP4: dmpq_sf_bytes(m, k) block scales; INT8: unused */
     const float* g;        /* NVFP4: device FP32 per-tensor scale g_a (input of the quantizer) */
     float* row_scale;      /* INT8: [m] per-token scale s = amax_row/127 (R2) */
@@ -154,6 +156,12 @@ double dmpq_derive_tau(double alpha, double beta, double tau_rel, double eps_slo
 dmpq_status dmpq_predict(const dmpq_block_stats* st, const double* tau_gamma, int n_layers, int t,
                          int prev_skipped, dmpq_gamma_metric metric, uint8_t* fmt_out, double* gamma_out);
 
+/* Purified Cache Refresh gate (R15), host-pure, applied after
+ * dmpq_predict: for each layer j, ratio[j] > tau_outlier (strict; 25) routes
+ * BF16 (no quantization); else prev_skipped routes INT8; else fmt_inout[j] stays.
+ * ratio may be NULL (no outlier gate). */
+void dmpq_purify(const double* ratio, int n_layers, int prev_skipped, double tau_outlier, uint8_t* fmt_inout);
+
 /* ========================================================================== */
 /* 3. dmpq_quantize_act                                                       */
 /* ========================================================================== */
@@ -168,6 +176,9 @@ typedef struct {
     float ln_eps;          /* DMPQ_QF_LAYERNORM epsilon (e.g. 1e-6) */
     uint16_t* h_out;       /* DMPQ_QF_WRITE_H: bf16 [m x k], row stride ldh */
     int ldh;
+    float* row_abs_sum;    /* optional [m]: sum_k |x| per row of the layer input (after LN, before any
+                              rotation), FP32 in a fixed order -- PDR outlier statistics (R15) */
+    float* amax_in;        /* optional device scalar: max(*amax_in, max |x|) of that input (R15) */
 } dmpq_quant_opts;
 
 /* Online activation quantization of X (bf16 [m x k], row stride ldx) into one or
@@ -179,7 +190,8 @@ typedef struct {
  *    max(fl(amax_{t-1}/1344), FLT_MIN)). Scale rows in [m, ceil128(m)) are zeroed.
  *  INT8 per token (R2): a = max_k|x|; s = fl(a/127); code =
  *    RNE(fl(x*fl(127/a))); a == 0 gives s = 1 and zero codes.
- *  Either output may be NULL, not both; out->m/k must equal m/k.
+ *  Either output may be NULL; both may be NULL when opts asks for h_out or the PDR
+ *  statistics only (a BF16-routed tensor, R15). out->m/k must equal m/k.
  *  amax_out: if non-NULL, device FP32 that receives max(*amax_out, max|x|)
  *  (atomic; the caller zeroes it once per step). With DMPQ_QF_LAYERNORM the
  *  quantised (and amax'd) values are the bf16-rounded normalised rows.
@@ -188,6 +200,10 @@ typedef struct {
  *  Shapes: k % 64 == 0 (k % 128 == 0 with DMPQ_QF_HADAMARD), 0 < k <= 16384, m >= 0. */
 dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
                               dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s);
+
+/* FP64 totals of per-row sums for the PDR outlier ratio (R15): out[s] = sum_r
+ * row_sums[s*m + r] for s < segments, fixed order (deterministic). */
+dmpq_status dmpq_outlier_reduce(const float* row_sums, int m, int segments, double* out, dmpq_stream_t s);
 
 /* Device-side global scale for the next NVFP4 quantization (R3):
  * g_out[i] = max(fl(amax[i] / div), FLT_MIN) for i < count (div = 2688 for a
@@ -210,6 +226,8 @@ typedef struct {
 } dmpq_epilogue;
 
 /* Y = A @ W^T with the dequant/bias epilogue (north_star), on tcgen05.
+ *  BF16  (kind::f16, R15): acc = sum_k a*w in the tensor core's FP32 accumulator;
+ *        y = fl(acc + bias[n]); needs W->bf16_w.
  *  INT8  (kind::i8): acc = sum_k a*w exactly in int32 (TMEM);
  *        y = fma(fl(float(acc) * s_a[m]), s_w[n], bias[n])             (R8)
  *  NVFP4 (kind::mxf4nvf4.block_scale.scale_vec::4X): acc = sum_k

@@ -22,8 +22,10 @@ import subprocess
 import numpy as np
 
 from .decisions import (  # noqa: F401  (re-export)
+    FMT_BF16,
     FMT_INT8,
     FMT_NVFP4,
+    purify_route,
     TdcConfig,
     TdcState,
     derive_tau_gamma,
@@ -77,6 +79,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_gemm_int8.argtypes, L.oracle_gemm_int8.restype = [P, P, P, P, P, I, I, I, I, I, P, P], I
         L.oracle_gemm_nvfp4.argtypes = [P, P, F, P, P, F, P, I, I, I, I, I, P]
         L.oracle_block_stats.argtypes = [P, P, P, LL, P, P]
+        L.oracle_gemm_bf16.argtypes = [P, P, P, I, I, I, I, I, P]
+        L.oracle_outlier_ratio.argtypes, L.oracle_outlier_ratio.restype = [P, LL, LL], ctypes.c_double
         L.oracle_tdc_skip.argtypes = [P, P, LL, P]
         L.oracle_amax_bf16.argtypes, L.oracle_amax_bf16.restype = [P, LL], F
         _lib = L
@@ -286,6 +290,25 @@ def gemm_nvfp4(a_codes, a_sf, g_a, w_codes, w_sf, g_w, bias, rows=None) -> np.nd
                             _p(w_codes), _p(np.ascontiguousarray(w_sf, dtype=np.uint8)), float(g_w),
                             _p(b), m, n, k, r0, r1, _p(y))
     return y
+
+
+def gemm_bf16(x_bf16, w_bf16, bias, rows=None) -> np.ndarray:
+    """BF16 fallback GEMM of the PDR gate (R15), fp64 accumulation."""
+    x = _u16(x_bf16)
+    w = _u16(w_bf16)
+    m, k = x.shape
+    n = w.shape[0]
+    r0, r1 = (0, m) if rows is None else rows
+    y = np.zeros((r1 - r0, n), dtype=np.float64)
+    b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    lib().oracle_gemm_bf16(_p(x), _p(w), _p(b), m, n, k, r0, r1, _p(y))
+    return y
+
+
+def outlier_ratio(x_bf16, stride: int = 1) -> float:
+    """R_outlier = max|X| / mean|X| (P:241; S:405-411)."""
+    x = _u16(x_bf16).reshape(-1)
+    return float(lib().oracle_outlier_ratio(_p(x), x.size, stride))
 
 
 def block_stats(x_in, x_out, delta_prev=None):

@@ -17,6 +17,7 @@ from dataclasses import dataclass, field
 
 FMT_INT8 = 0
 FMT_NVFP4 = 1
+FMT_BF16 = 2
 
 COMPUTE = 0
 SKIP = 1
@@ -56,6 +57,18 @@ def route_block(gamma: float | None, tau_gamma, t: int, prev_skipped: bool):
         else:
             out.append(FMT_NVFP4)
     return out
+
+
+def purify_route(base, ratio: float | None, prev_skipped: bool, tau_outlier: float = 25.0):
+    """Purified Cache Refresh, per layer: an outlier ratio strictly
+    above tau_outlier routes the layer to full precision (BF16); otherwise the first
+    compute after a Skip routes INT8; otherwise the DMPQ decision stands.
+    Precedence outlier > post-skip > base."""
+    if ratio is not None and ratio > tau_outlier:
+        return FMT_BF16
+    if prev_skipped:
+        return FMT_INT8
+    return base
 
 
 def cosine_error_from_stats(dot: float, n_new: float, n_prev: float) -> float:

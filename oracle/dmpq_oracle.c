@@ -431,6 +431,38 @@ void oracle_gemm_nvfp4(const uint8_t* a_codes, const uint8_t* a_sf, float g_a,
         }
 }
 
+/* BF16 full-precision fallback GEMM ("uses full precision (FP16/BF16)",
+ * reading R15): Y = sum_k x*w + bias with bf16 x, w, in fp64 (bf16 products are exact). */
+void oracle_gemm_bf16(const uint16_t* x, const uint16_t* w, const float* bias, int m, int n, int k,
+                      int row0, int row1, double* y_out) {
+    (void)m;
+    for (int i = row0; i < row1; ++i)
+        for (int j = 0; j < n; ++j) {
+            double acc = 0.0;
+            for (int t = 0; t < k; ++t)
+                acc += (double)oracle_bf16_to_f32(x[(size_t)i * k + t]) * (double)oracle_bf16_to_f32(w[(size_t)j * k + t]);
+            if (bias) acc += (double)bias[j];
+            y_out[(size_t)(i - row0) * n + j] = acc;
+        }
+}
+
+/* Outlier ratio of the Purified Cache Refresh gate: R = max|X| / mean|X|
+ * over every `stride`-th element (stride 1 = exact). An all-zero sample has
+ * ratio 1. */
+double oracle_outlier_ratio(const uint16_t* x, long long count, long long stride) {
+    double mx = 0.0;
+    long double s = 0.0L;
+    long long n = 0;
+    for (long long i = 0; i < count; i += stride) {
+        double v = fabs((double)oracle_bf16_to_f32(x[i]));
+        if (v > mx) mx = v;
+        s += v;
+        ++n;
+    }
+    if (s == 0.0L) return 1.0;
+    return mx / (double)(s / (long double)n);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Block statistics for the predictor and TDC (one pass definitions).          */
 /*   d_i = fl32(y_i - x_i)                         (Eq. 8: X_out = X_in + Delta) */

@@ -18,7 +18,7 @@ c_int, c_float, c_double, c_void_p, c_uint32, c_size_t = (
 DMPQ_OK, DMPQ_EINVAL, DMPQ_ESHAPE, DMPQ_EALIGN, DMPQ_EZERONORM, DMPQ_ECUDA, DMPQ_EUNSUPPORTED = range(7)
 STATUS_NAMES = ["DMPQ_OK", "DMPQ_EINVAL", "DMPQ_ESHAPE", "DMPQ_EALIGN", "DMPQ_EZERONORM", "DMPQ_ECUDA",
                 "DMPQ_EUNSUPPORTED"]
-FMT_INT8, FMT_NVFP4 = 0, 1
+FMT_INT8, FMT_NVFP4, FMT_BF16 = 0, 1, 2
 QF_LAYERNORM, QF_WRITE_H, QF_HADAMARD = 1, 2, 4
 PACK_HADAMARD = 1
 EP_BIAS, EP_GELU_TANH, EP_RESIDUAL = 1, 2, 4
@@ -30,7 +30,7 @@ STATS_LEN = 7
 
 class Weights(ctypes.Structure):
     _fields_ = [("n", c_int), ("k", c_int), ("fp4_codes", c_void_p), ("fp4_sf", c_void_p), ("fp4_g", c_void_p),
-                ("i8_codes", c_void_p), ("i8_scale", c_void_p), ("bias", c_void_p)]
+                ("i8_codes", c_void_p), ("i8_scale", c_void_p), ("bias", c_void_p), ("bf16_w", c_void_p)]
 
 
 class Act(ctypes.Structure):
@@ -39,7 +39,8 @@ class Act(ctypes.Structure):
 
 
 class QuantOpts(ctypes.Structure):
-    _fields_ = [("flags", c_uint32), ("ln_eps", c_float), ("h_out", c_void_p), ("ldh", c_int)]
+    _fields_ = [("flags", c_uint32), ("ln_eps", c_float), ("h_out", c_void_p), ("ldh", c_int),
+                ("row_abs_sum", c_void_p), ("amax_in", c_void_p)]
 
 
 class Epilogue(ctypes.Structure):
@@ -80,6 +81,8 @@ _SIGNATURES = {
     "dmpq_quantize_act": ([c_void_p, c_int, c_int, c_int, ctypes.POINTER(QuantOpts), ctypes.POINTER(Act),
                            ctypes.POINTER(Act), c_void_p, c_void_p], c_int),
     "dmpq_global_scale": ([c_void_p, c_float, c_void_p, c_int, c_void_p], c_int),
+    "dmpq_outlier_reduce": ([c_void_p, c_int, c_int, c_void_p, c_void_p], c_int),
+    "dmpq_purify": ([ctypes.POINTER(c_double), c_int, c_int, c_double, ctypes.POINTER(ctypes.c_uint8)], None),
     "dmpq_gemm": ([ctypes.POINTER(Act), ctypes.POINTER(Weights), ctypes.POINTER(Epilogue), c_void_p, c_int, c_void_p,
                    c_void_p, c_void_p], c_int),
     "tdc_step": ([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p], c_int),

@@ -35,6 +35,7 @@ from . import synth
 from .shard import exchange
 
 LAYERS = ("q", "k", "v", "o", "ffn1", "ffn2")
+N_STATS = L.STATS_LEN + 4      # per block: 7 TDC/predictor sums + sum|x| of the 4 layer inputs (PDR, R15)
 SLOT_OF_LAYER = (0, 0, 0, 1, 2, 3)   # activation tensor each layer consumes
 N_SLOTS = 4
 
@@ -56,7 +57,8 @@ class BlockWeights:
         return sum(w.nbytes() for w in self.layers)
 
 
-def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, hadamard: bool = False) -> BlockWeights:
+def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, hadamard: bool = False,
+                       keep_bf16: bool = False) -> BlockWeights:
     shapes = [(H, H), (H, H), (H, H), (H, H), (F, H), (H, F)]
     layers = []
     for j, (n, k) in enumerate(shapes):
@@ -64,8 +66,9 @@ def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, had
             w, b = synth.linear_weight_device(n, k, seed * 16 + j, device)
         else:
             w, b = synth.linear_weight(n, k, seed * 16 + j)
-        layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard))
-        del w
+        layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard, keep_bf16=keep_bf16))
+        if not keep_bf16:
+            del w
     g = torch.Generator(device="cpu")
     g.manual_seed(seed * 16 + 15)
     g1 = (gate_scale * (0.5 + torch.rand(H, generator=g))).to(device)
@@ -89,6 +92,8 @@ class Workspace:
             self.acts[(slot, D.FMT_INT8)] = D.QuantAct.empty(D.FMT_INT8, m, k, device)
             self.acts[(slot, D.FMT_NVFP4)] = D.QuantAct.empty(D.FMT_NVFP4, m, k, device, g=g_table[0, slot:slot + 1])
         self.tdc_ws = torch.zeros(D.tdc_workspace_bytes(m, H), dtype=torch.uint8, device=device)
+        self.h1 = torch.empty(m, H, **e)          # LN outputs, materialised only for BF16-routed layers (R15)
+        self.h2 = torch.empty(m, H, **e)
 
     def act(self, slot: int, fmt: int, block: int) -> D.QuantAct:
         a = self.acts[(slot, fmt)]
@@ -113,7 +118,8 @@ class DiTStack:
 
     def __init__(self, n_blocks: int, H: int, F: int, m_local: int, device, seed: int = 0,
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
-                 force_fmt: int | None = None, group=None, hadamard: bool = False):
+                 force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
+                 tau_outlier: float = 25.0, m_total: int | None = None):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -122,18 +128,24 @@ class DiTStack:
         self.force_fmt = force_fmt
         self.group = group
         self.hadamard = hadamard      # online block-Hadamard smoothing (R14)
+        self.pdr = pdr                # Purified Cache Refresh outlier gate (R15)
+        self.tau_outlier = tau_outlier
+        self.m_total = m_total if m_total is not None else m_local
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
-        self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard)
+        self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr)
                        for b in range(n_blocks)]
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
-        self.amax = torch.zeros(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
+        # [:, :4] amax of the quantised values (NVFP4 global scales, R3); [:, 4:] max|x| of the layer inputs (PDR)
+        self.amax = torch.zeros(n_blocks, 2 * N_SLOTS, dtype=torch.float32, device=self.device)
+        self.row_abs = torch.zeros(n_blocks * N_SLOTS, m_local, dtype=torch.float32, device=self.device)
         self.ws = Workspace(m_local, H, F, self.device, self.g_table)
         self.delta = [torch.zeros(m_local, H, dtype=torch.bfloat16, device=self.device) for _ in range(n_blocks)]
         world = 1 if group is None else torch.distributed.get_world_size(group)
         self.world = world
         self.rank = 0 if group is None else torch.distributed.get_rank(group)
-        self.stats_slots = torch.zeros(world, n_blocks, L.STATS_LEN, dtype=torch.float64, device=self.device)
+        self.stats_slots = torch.zeros(world, n_blocks, N_STATS, dtype=torch.float64, device=self.device)
+        self.ratio = [None] * n_blocks          # PDR outlier ratio per slot from the block's last compute
         self.x_buf = [torch.empty(m_local, H, dtype=torch.bfloat16, device=self.device) for _ in range(2)]
         self.tdc = [D.tdc_new_state() for _ in range(n_blocks)]
         self.prev_stats = [None] * n_blocks     # global stats of the block's last step (None if skipped)
@@ -141,9 +153,10 @@ class DiTStack:
         self.records: list[StepRecord] = []
         self.launches = 0                       # libdmpq kernel launches issued (bench's gpu_launches)
         self.timing = False                     # record CUDA events around every GEMM (roofline)
-        self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: []}
-        self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0}
+        self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
+        self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
         self.capture = None                     # dict -> per-stage clones for the parity tests
+        self.pdr_sums = torch.zeros(n_blocks * N_SLOTS, dtype=torch.float64, device=self.device)
 
     def _cap(self, key, t):
         if self.capture is not None:
@@ -159,45 +172,51 @@ class DiTStack:
             self.capture[key] = d
 
     # ------------------------------------------------------------------ one block
+    def _quant(self, b, slot, src, fmts_needed, layernorm=False, h_buf=None):
+        """Quantize one activation tensor into the formats its consumers need (plus PDR
+        statistics); returns {fmt: QuantAct} with FMT_BF16 -> the bf16 tensor itself."""
+        ws = self.ws
+        want_h = layernorm and (D.FMT_BF16 in fmts_needed or self.capture is not None)
+        a8 = ws.act(slot, D.FMT_INT8, b) if D.FMT_INT8 in fmts_needed else None
+        a4 = ws.act(slot, D.FMT_NVFP4, b) if D.FMT_NVFP4 in fmts_needed else None
+        D.dmpq_quantize_act(src, out_i8=a8, out_fp4=a4, amax_out=self.amax[b, slot:slot + 1], layernorm=layernorm,
+                            h_out=h_buf if want_h else None, hadamard=self.hadamard,
+                            row_abs_sum=self.row_abs[b * N_SLOTS + slot] if self.pdr else None,
+                            amax_in=self.amax[b, N_SLOTS + slot:N_SLOTS + slot + 1] if self.pdr else None)
+        out = {D.FMT_INT8: a8, D.FMT_NVFP4: a4}
+        if D.FMT_BF16 in fmts_needed:
+            out[D.FMT_BF16] = D.QuantAct.bf16(h_buf if layernorm else src)
+        return out
+
     def _compute_block(self, b: int, x_in: torch.Tensor, x_out: torch.Tensor, fmts) -> float:
         W, ws, H, F, m = self.blocks[b], self.ws, self.H, self.F, self.m
-        amax = self.amax[b]
-        # attention input: LN fused into the quantizer, one pass for both formats if mixed
-        need = set(fmts[0:3])
-        a0_i8 = ws.act(0, D.FMT_INT8, b) if D.FMT_INT8 in need else None
-        a0_f4 = ws.act(0, D.FMT_NVFP4, b) if D.FMT_NVFP4 in need else None
         cap = self.capture is not None
-        h1 = torch.empty(m, H, dtype=torch.bfloat16, device=x_in.device) if cap else None
-        hd = self.hadamard
-        D.dmpq_quantize_act(x_in, out_i8=a0_i8, out_fp4=a0_f4, amax_out=amax[0:1], layernorm=True, h_out=h1, hadamard=hd)
+        # attention input: LN fused into the quantizer, one pass for every format Q/K/V need
+        q0 = self._quant(b, 0, x_in, set(fmts[0:3]), layernorm=True, h_buf=ws.h1)
         if cap:
-            self._cap("x_in", x_in); self._cap("h1", h1)
-            self._cap_act("a0_i8", a0_i8); self._cap_act("a0_f4", a0_f4)
+            self._cap("x_in", x_in); self._cap("h1", ws.h1)
+            self._cap_act("a0_i8", q0[D.FMT_INT8]); self._cap_act("a0_f4", q0[D.FMT_NVFP4])
         for j, out in ((0, ws.qk), (1, ws.qk), (2, ws.v)):
-            a = a0_i8 if fmts[j] == D.FMT_INT8 else a0_f4
-            self._gemm(a, W.layers[j], Y=out)
+            self._gemm(q0[fmts[j]], W.layers[j], Y=out)
             self._cap(f"y{j}", out)
         # O projection on the attention stand-in a = v, gated residual in the epilogue
-        a1 = ws.act(1, fmts[3], b)
-        D.dmpq_quantize_act(ws.v, **{("out_i8" if fmts[3] == D.FMT_INT8 else "out_fp4"): a1}, amax_out=amax[1:2],
-                            hadamard=hd)
-        self._cap_act("a1", a1)
-        self._gemm(a1, W.layers[3], Y=ws.x_mid, residual=x_in, gate=W.g1)
+        q1 = self._quant(b, 1, ws.v, {fmts[3]})
+        if fmts[3] != D.FMT_BF16:
+            self._cap_act("a1", q1[fmts[3]])
+        self._gemm(q1[fmts[3]], W.layers[3], Y=ws.x_mid, residual=x_in, gate=W.g1)
         self._cap("x_mid", ws.x_mid)
         # FFN
-        a2 = ws.act(2, fmts[4], b)
-        h2 = torch.empty(m, H, dtype=torch.bfloat16, device=x_in.device) if cap else None
-        D.dmpq_quantize_act(ws.x_mid, **{("out_i8" if fmts[4] == D.FMT_INT8 else "out_fp4"): a2},
-                            amax_out=amax[2:3], layernorm=True, h_out=h2, hadamard=hd)
+        q2 = self._quant(b, 2, ws.x_mid, {fmts[4]}, layernorm=True, h_buf=ws.h2)
         if cap:
-            self._cap("h2", h2); self._cap_act("a2", a2)
-        self._gemm(a2, W.layers[4], Y=ws.f, gelu=True)
+            self._cap("h2", ws.h2)
+            if fmts[4] != D.FMT_BF16:
+                self._cap_act("a2", q2[fmts[4]])
+        self._gemm(q2[fmts[4]], W.layers[4], Y=ws.f, gelu=True)
         self._cap("f", ws.f)
-        a3 = ws.act(3, fmts[5], b)
-        D.dmpq_quantize_act(ws.f, **{("out_i8" if fmts[5] == D.FMT_INT8 else "out_fp4"): a3}, amax_out=amax[3:4],
-                            hadamard=hd)
-        self._cap_act("a3", a3)
-        self._gemm(a3, W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
+        q3 = self._quant(b, 3, ws.f, {fmts[5]})
+        if fmts[5] != D.FMT_BF16:
+            self._cap_act("a3", q3[fmts[5]])
+        self._gemm(q3[fmts[5]], W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
         self._cap("x_out", x_out)
         self.launches += 4 + 6
         return 2.0 * m * (4 * H * H + 2 * H * F)
@@ -221,8 +240,8 @@ class DiTStack:
         return out
 
     def reset_timing(self):
-        self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: []}
-        self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0}
+        self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
+        self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
 
     # ------------------------------------------------------------------ one timestep
     def step(self, x0: torch.Tensor, t: int) -> torch.Tensor:
@@ -245,8 +264,11 @@ class DiTStack:
                     fmts, gamma = [self.force_fmt] * 6, float("nan")
                 else:
                     fmts, gamma, _ = D.dmpq_predict(self.prev_stats[b], self.tau, t, self.prev_skipped[b])
+                    if self.pdr and self.ratio[b] is not None:
+                        fmts = D.dmpq_purify(fmts, [self.ratio[b][s] for s in SLOT_OF_LAYER], self.prev_skipped[b],
+                                             self.tau_outlier)
                 rec.linear_flops += self._compute_block(b, x_in, x_out, fmts)
-                D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b],
+                D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
                            self.ws.tdc_ws)
                 self.launches += 1
                 rec.fmts.append(fmts)
@@ -260,10 +282,16 @@ class DiTStack:
         """Per-step exchange + host decisions: combine the statistics of all ranks
         (slot-packed SUM all-reduce = exact all-gather; MAX all-reduce for amax), copy
         them to the host once, update TDC (Eq. 10) and the NVFP4 global scales (R3)."""
+        if self.pdr:   # per-slot sum|x| of this rank's rows -> its stats slot (FP64, fixed order)
+            D.dmpq_outlier_reduce(self.row_abs, self.pdr_sums)
+            self.stats_slots[self.rank, :, L.STATS_LEN:] = self.pdr_sums.view(self.nb, N_SLOTS)
+            self.launches += 1
         # one exchange per step; the D2H copy inside synchronises the stream
         stats = exchange(self.stats_slots, self.amax, self.group, self.world)
-        D.dmpq_global_scale(self.amax.view(-1), 1344.0, self.g_table.view(-1))
+        D.dmpq_global_scale(self.amax[:, :N_SLOTS].contiguous().view(-1), 1344.0, self.g_table.view(-1))
         self.launches += 1
+        if self.pdr:
+            amax_in = self.amax[:, N_SLOTS:].cpu().numpy().astype(np.float64)
         rec = self.records[-1]
         for b in range(self.nb):
             d = rec.decisions[b]
@@ -272,16 +300,20 @@ class DiTStack:
                 self.prev_stats[b] = None
                 self.prev_skipped[b] = True
             else:
-                st = L.BlockStats.from_seq(stats[b])
+                st = L.BlockStats.from_seq(stats[b][:L.STATS_LEN])
                 D.tdc_update(self.tdc[b], self.cfg, t, d, st)
                 self.prev_stats[b] = st
                 self.prev_skipped[b] = False
+                if self.pdr:   # R = max|x| / mean|x| of each layer input over all tokens (R15)
+                    ks = (self.H, self.H, self.H, self.F)
+                    self.ratio[b] = [float(amax_in[b, s]) / (stats[b][L.STATS_LEN + s] / (self.m_total * ks[s]))
+                                     if stats[b][L.STATS_LEN + s] > 0 else 1.0 for s in range(N_SLOTS)]
         return stats
 
     def mix(self, records=None):
         """Realised NVFP4 / INT8 / skip mix over the given step records."""
         records = self.records if records is None else records
-        n4 = n8 = sk = 0
+        n4 = n8 = n16 = sk = 0
         for r in records:
             for f in r.fmts:
                 if f is None:
@@ -289,6 +321,8 @@ class DiTStack:
                 else:
                     n4 += sum(1 for x in f if x == D.FMT_NVFP4)
                     n8 += sum(1 for x in f if x == D.FMT_INT8)
-        tot_layers = max(1, n4 + n8)
+                    n16 += sum(1 for x in f if x == D.FMT_BF16)
+        tot_layers = max(1, n4 + n8 + n16)
         nblk = max(1, sum(len(r.fmts) for r in records))
-        return {"nvfp4_layer_frac": n4 / tot_layers, "int8_layer_frac": n8 / tot_layers, "skip_block_frac": sk / nblk}
+        return {"nvfp4_layer_frac": n4 / tot_layers, "int8_layer_frac": n8 / tot_layers,
+                "bf16_layer_frac": n16 / tot_layers, "skip_block_frac": sk / nblk}

@@ -1,6 +1,8 @@
 // gemm.cu — dmpq_gemm: the DMPQ linear layer on 5th-generation tensor cores.
 //   INT8  : tcgen05.mma.kind::i8, exact int32 accumulation in TMEM, FP32
 //           per-token x per-channel dequant epilogue, bit-exact (R8).
+//   BF16  : tcgen05.mma.kind::f16 (BF16 x BF16 -> FP32), the full-precision fallback of
+//           the Purified Cache Refresh outlier gate (R15).
 //   NVFP4 : tcgen05.mma.kind::mxf4nvf4.block_scale.scale_vec::4X, E4M3 block scales
 //           staged smem -> TMEM with tcgen05.cp, FP32 accumulation in TMEM,
 //           per-tensor g_a*g_w dequant fused with the bias as one FMA (R3).
@@ -65,8 +67,9 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8
 // mainloop of tile i+1). Epilogue: TMEM -> registers -> 64B-swizzled smem staging
 // -> TMA store; per-column vectors (bias, w_scale, gate) staged in smem per tile.
 // ============================================================================
-template <bool FP4, int BN, int STAGES>
+template <int KIND, int BN, int STAGES>   // KIND: 0 INT8, 1 NVFP4, 2 BF16
 struct PairLayout {
+    static constexpr bool FP4 = KIND == 1;
     static constexpr int A_BYTES = BM * BK_BYTES;                 // 16 KB
     static constexpr int B_BYTES = (BN / 2) * BK_BYTES;           // this CTA's half of B
     static constexpr int SFA_BYTES = FP4 ? 4 * 512 : 0;
@@ -82,12 +85,14 @@ struct PairLayout {
     static_assert(STAGE_BYTES % 1024 == 0, "stage buffers must stay 1024-B aligned");
 };
 
-template <bool FP4, int BN, int STAGES>
+template <int KIND, int BN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     dmpq_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
-    using L = PairLayout<FP4, BN, STAGES>;
+    using L = PairLayout<KIND, BN, STAGES>;
+    constexpr bool FP4 = KIND == 1;
+    constexpr bool I8 = KIND == 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -165,7 +170,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const uint32_t sfb_t = sfa_t + 16;
             uint32_t idesc;
             if constexpr (FP4) idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-            else idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            else if constexpr (I8) idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            else idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);  // F32 acc, BF16 x BF16
             for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
                 const int nt = tile % p.num_n_tiles;
                 const int acc = local & 1;
@@ -198,8 +204,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                             const uint32_t accum = (kb | j) ? 1u : 0u;
                             if constexpr (FP4)
                                 mma_fp4_pair(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, sfa_t + j * 4, sfb_t + j * 8 + sfb_shift, accum);
-                            else
+                            else if constexpr (I8)
                                 mma_i8_pair(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, accum);
+                            else
+                                mma_f16_pair(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, accum);
                         }
                         tc_commit_pair_mc(bar_empty + 8 * stage, 0x3);
                     }
@@ -222,6 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         uint32_t chunk_ctr = 0;
         float gg = 0.0f;
         if constexpr (FP4) gg = __fmul_rn(*p.g_a, *p.g_w);
+        else if constexpr (!I8) gg = 1.0f;   // BF16: y = fma(acc, 1, bias) = fl(acc + bias)
         const f2 gg2 = f2make(gg, gg);
         const uint32_t staging = sbase + L::STAGING_OFFSET + q * 4096;
         const uint32_t vec_s = sbase + L::VEC_OFFSET;
@@ -239,7 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 const int col = n0 + i;
                 const bool ok = col < p.n;
                 const float bv = (ok && has_bias) ? p.bias[col] : -0.0f;   // fma(x, s, -0) == fl(x * s) exactly
-                const float wv = (!FP4 && ok) ? p.w_scale[col] : 0.0f;
+                const float wv = (I8 && ok) ? p.w_scale[col] : 0.0f;
                 const float gv = (ok && has_res) ? p.gate[col] : 0.0f;
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + i * 4), "f"(bv) : "memory");
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + (BN + i) * 4), "f"(wv) : "memory");
@@ -250,7 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const int row = rowbase + lane;
             const bool row_ok = row < p.m;
             float sa = 0.0f;
-            if constexpr (!FP4) sa = row_ok ? p.a_scale[row] : 0.0f;
+            if constexpr (I8) sa = row_ok ? p.a_scale[row] : 0.0f;
             const f2 sa2 = f2make(sa, sa);
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
             tc_fence_after();
@@ -273,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                  : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(vb + (c * 32 + v4 * 4) * 4));
                     const f2 bb0 = f2make(b0, b1), bb1 = f2make(b2, b3);
-                    if constexpr (FP4) {
+                    if constexpr (!I8) {
                         const f2 a0 = f2make(__uint_as_float(r[4 * v4]), __uint_as_float(r[4 * v4 + 1]));
                         const f2 a1 = f2make(__uint_as_float(r[4 * v4 + 2]), __uint_as_float(r[4 * v4 + 3]));
                         // y = fma(acc, g_a*g_w, bias): one rounding (FP32 tolerance path, R3)
@@ -345,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                         for (int v4 = 0; v4 < 8; ++v4)
                             yp[v4] = make_float4(f2lo(y[2 * v4]), f2hi(y[2 * v4]), f2lo(y[2 * v4 + 1]), f2hi(y[2 * v4 + 1]));
                     }
-                    if constexpr (!FP4) {
+                    if constexpr (I8) {
                         if (p.acc_out) {
                             int4* ap = reinterpret_cast<int4*>(p.acc_out + (size_t)row * p.n + col0);
 #pragma unroll
@@ -421,9 +430,10 @@ static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, i
     return r == CUDA_SUCCESS;
 }
 
-template <bool FP4, int BN, int STAGES>
+template <int KIND, int BN, int STAGES>
 static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
-    using L = PairLayout<FP4, BN, STAGES>;
+    using L = PairLayout<KIND, BN, STAGES>;
+    constexpr bool FP4 = KIND == 1;
     CUtensorMap tmA, tmB, tmSFA, tmSFB, tmY;
     std::memset(&tmSFA, 0, sizeof(tmSFA));
     std::memset(&tmSFB, 0, sizeof(tmSFB));
@@ -440,7 +450,7 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     p.num_m_tiles = (p.m + 255) / 256;
     p.num_n_tiles = (p.n + BN - 1) / BN;
     p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
-    auto kern = dmpq_gemm_pair_kernel<FP4, BN, STAGES>;
+    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
@@ -461,7 +471,8 @@ using namespace dmpq;
 extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const dmpq_epilogue* ep, uint16_t* Y, int ldy,
                                  float* Y32, int32_t* acc_or_null, dmpq_stream_t s) {
     DMPQ_REQUIRE(A && W, DMPQ_EINVAL, "dmpq_gemm: NULL operand");
-    DMPQ_REQUIRE(A->fmt == DMPQ_FMT_INT8 || A->fmt == DMPQ_FMT_NVFP4, DMPQ_EINVAL, "dmpq_gemm: unknown format");
+    DMPQ_REQUIRE(A->fmt == DMPQ_FMT_INT8 || A->fmt == DMPQ_FMT_NVFP4 || A->fmt == DMPQ_FMT_BF16, DMPQ_EINVAL,
+                 "dmpq_gemm: unknown format");
     const bool fp4 = A->fmt == DMPQ_FMT_NVFP4;
     const int m = A->m, n = W->n, k = A->k;
     DMPQ_REQUIRE(k == W->k && k > 0 && k % 64 == 0 && n > 0 && n % 32 == 0 && m >= 0, DMPQ_ESHAPE,
@@ -495,12 +506,17 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
-        return launch_gemm_pair<true, 192, 6>(p, A->codes, W->fp4_codes, st);
+        return launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
+    } else if (A->fmt == DMPQ_FMT_BF16) {
+        DMPQ_REQUIRE(A->codes && W->bf16_w && aligned16(A->codes) && aligned16(W->bf16_w), DMPQ_EALIGN,
+                     "dmpq_gemm: BF16 path needs A->codes (bf16 activation) and W->bf16_w");
+        p.kbytes = 2 * k;
+        return launch_gemm_pair<2, 256, 6>(p, A->codes, W->bf16_w, st);
     } else {
         DMPQ_REQUIRE(A->codes && A->row_scale && W->i8_codes && W->i8_scale && aligned16(A->codes) && aligned16(W->i8_codes),
                      DMPQ_EALIGN, "dmpq_gemm: INT8 operand pointers");
         p.kbytes = k;
         p.a_scale = A->row_scale; p.w_scale = W->i8_scale;
-        return launch_gemm_pair<false, 256, 6>(p, A->codes, W->i8_codes, st);
+        return launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);
     }
 }

@@ -96,6 +96,13 @@ extern "C" dmpq_status dmpq_predict(const dmpq_block_stats* st, const double* ta
     return rc;
 }
 
+extern "C" void dmpq_purify(const double* ratio, int n_layers, int prev_skipped, double tau_outlier, uint8_t* fmt_inout) {
+    for (int j = 0; j < n_layers; ++j) {
+        if (ratio && ratio[j] > tau_outlier) fmt_inout[j] = (uint8_t)DMPQ_FMT_BF16;
+        else if (prev_skipped) fmt_inout[j] = (uint8_t)DMPQ_FMT_INT8;
+    }
+}
+
 extern "C" void tdc_init(tdc_state* st) {
     st->t_p = -1;
     st->e_tp = INFINITY;

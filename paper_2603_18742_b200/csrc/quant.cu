@@ -25,6 +25,8 @@ struct QuantParams {
     uint8_t* fp4_sf;
     const float* g;
     float* amax_out;
+    float* row_abs_sum;   // PDR statistics (R15): per-row sum |x| of the layer input (pre-rotation)
+    float* amax_in;       //                       max |x| of the layer input (pre-rotation)
     int kc4;     // scale-column atoms per 128-row tile: ceil(k/16/4)
     int m_pad;   // rows rounded up to 128 (scale rows to zero-fill)
 };
@@ -38,7 +40,7 @@ struct QuantParams {
 // lanes (tid ^ 1). Group reductions: warp shuffles, then smem + a named barrier per group.
 // ---------------------------------------------------------------------------------------------
 struct GroupReduce {
-    float* red;      // [6 areas][8 groups][8 warps]
+    float* red;      // [8 areas][8 groups][8 warps]
     int tpr, group, warp_in_group, lane;
     __device__ __forceinline__ float sum(float v, int area) {
         v = warp_sum(v);
@@ -150,7 +152,7 @@ __device__ __forceinline__ void load_chunks(uint4 (&v)[NC][8], const uint16_t* x
 
 template <int NC, bool HAD>
 __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams p, int tpr) {
-    __shared__ float red[6 * 8 * 8];
+    __shared__ float red[8 * 8 * 8];
     const int lane = threadIdx.x & 31;
     const int group = threadIdx.x / tpr, tid = threadIdx.x % tpr;
     const int groups = blockDim.x / tpr;
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
     const bool want_i8 = p.i8_codes != nullptr;
     const float g = want_fp4 ? *p.g : 1.0f;
     const int stride = gridDim.x * groups;
-    float my_amax = 0.0f;
+    float my_amax = 0.0f, my_amax_in = 0.0f;
     int parity = 0;
 
     int row = blockIdx.x * groups + group;
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
         const int next = row + stride;
         uint4 nv[NC][8];   // prefetch the next row while this one is processed
         load_chunks<NC>(nv, p.X + (size_t)next * p.ldx, tid, tpr, nch, next < p.m);
-        const int a0 = parity * 3;
+        const int a0 = parity * 4;
         if (p.flags & DMPQ_QF_LAYERNORM) {
             // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue, R13)
             f2 s2 = f2make(0.0f, 0.0f);
@@ -213,6 +215,24 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
                         *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)c * 64 + j * 8) = v[i][j];
                 }
             }
+        }
+        if (p.row_abs_sum || p.amax_in) {   // PDR outlier statistics of the layer input (R15)
+            float sa = 0.0f, mx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t w[4] = {v[i][j].x, v[i][j].y, v[i][j].z, v[i][j].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float lo = fabsf(bf16lo(w[t])), hi = fabsf(bf16hi(w[t]));
+                        sa = __fadd_rn(__fadd_rn(sa, lo), hi);
+                        mx = fmaxf(mx, fmaxf(lo, hi));
+                    }
+                }
+            my_amax_in = fmaxf(my_amax_in, mx);
+            const float rs = gr.sum(sa, a0 + 3);
+            if (tid == 0 && p.row_abs_sum) p.row_abs_sum[row] = rs;
         }
         // per-16-block |x| maxima (4 per chunk) and this thread's row maximum
         float bmax[NC][4];
@@ -337,6 +357,10 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
     if (p.amax_out) {
         const float am = warp_max(my_amax);
         if (lane == 0) atomic_max_nonneg(p.amax_out, am);
+    }
+    if (p.amax_in) {
+        const float am = warp_max(my_amax_in);
+        if (lane == 0) atomic_max_nonneg(p.amax_in, am);
     }
 }
 
@@ -486,6 +510,17 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
             tmax = fmaxf(tmax, vmax[i]);
         }
         cta_amax = fmaxf(cta_amax, tmax);
+        if (p.row_abs_sum) {   // PDR outlier statistics of the layer input (R15)
+            float sa = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) sa = __fadd_rn(__fadd_rn(sa, fabsf(bf16lo(w[t]))), fabsf(bf16hi(w[t])));
+            }
+            const float rs = rr.sum(sa);
+            if (tid == 0) p.row_abs_sum[row] = rs;
+        }
 
         if (want_fp4) {
             uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
@@ -539,9 +574,26 @@ __global__ void __launch_bounds__(256) quant_act_kernel(const QuantParams p) {
             *reinterpret_cast<uint32_t*>(sf_row + (size_t)c4 * 512) = 0u;
         }
     }
-    if (p.amax_out) {
+    if (p.amax_out || p.amax_in) {
         float am = warp_max(cta_amax);
-        if (lane == 0) atomic_max_nonneg(p.amax_out, am);
+        if (lane == 0 && p.amax_out) atomic_max_nonneg(p.amax_out, am);
+        if (lane == 0 && p.amax_in) atomic_max_nonneg(p.amax_in, am);   // unrotated: the same values
+    }
+}
+
+// Deterministic fixed-order FP64 sum of per-row sums: one CTA per segment.
+__global__ void __launch_bounds__(256) outlier_reduce_kernel(const float* rows, int m, double* out) {
+    __shared__ double red[8];
+    const float* r = rows + (size_t)blockIdx.x * m;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) s = __dadd_rn(s, (double)r[i]);
+    s = warp_sum_d(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = __dadd_rn(t, red[w]);
+        out[blockIdx.x] = t;
     }
 }
 
@@ -580,7 +632,9 @@ using namespace dmpq;
 
 extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
                                          dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s) {
-    DMPQ_REQUIRE(out_i8 || out_fp4, DMPQ_EINVAL, "dmpq_quantize_act: both outputs are NULL");
+    DMPQ_REQUIRE(out_i8 || out_fp4 ||
+                     (opts && ((opts->flags & DMPQ_QF_WRITE_H) || opts->row_abs_sum || opts->amax_in)),
+                 DMPQ_EINVAL, "dmpq_quantize_act: nothing to produce (no output, h_out or statistics)");
     DMPQ_REQUIRE(m >= 0 && k > 0 && k % 64 == 0 && k <= 16384, DMPQ_ESHAPE,
                  "dmpq_quantize_act: need k %% 64 == 0, 0 < k <= 16384, m >= 0 (m=%d k=%d)", m, k);
     DMPQ_REQUIRE(ldx >= k && ldx % 8 == 0, DMPQ_EALIGN, "dmpq_quantize_act: ldx=%d must be >= k and a multiple of 8", ldx);
@@ -614,6 +668,8 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
     p.fp4_sf = out_fp4 ? out_fp4->sf : nullptr;
     p.g = out_fp4 ? out_fp4->g : nullptr;
     p.amax_out = amax_out;
+    p.row_abs_sum = opts ? opts->row_abs_sum : nullptr;
+    p.amax_in = opts ? opts->amax_in : nullptr;
     p.kc4 = ((k / 16) + 3) / 4;
     p.m_pad = (m + 127) / 128 * 128;
     if (m == 0) return DMPQ_OK;
@@ -645,6 +701,14 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
         }
     }
     return check_launch("dmpq_quantize_act");
+}
+
+extern "C" dmpq_status dmpq_outlier_reduce(const float* row_sums, int m, int segments, double* out, dmpq_stream_t s) {
+    DMPQ_REQUIRE(row_sums && out && m >= 0 && segments >= 0, DMPQ_EINVAL, "dmpq_outlier_reduce: bad arguments");
+    if (segments == 0) return DMPQ_OK;
+    DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_outlier_reduce: needs an sm_100 device");
+    outlier_reduce_kernel<<<segments, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(row_sums, m, out);
+    return check_launch("dmpq_outlier_reduce");
 }
 
 extern "C" dmpq_status dmpq_global_scale(const float* amax, float div, float* g_out, int count, dmpq_stream_t s) {

@@ -17,10 +17,10 @@ from . import _lib as L
 __all__ = [
     "PackedWeights", "QuantAct", "dmpq_pack_weights", "dmpq_predict", "dmpq_derive_tau", "dmpq_quantize_act",
     "dmpq_global_scale", "dmpq_gemm", "tdc_step", "tdc_decide", "tdc_update", "tdc_new_state", "sf_bytes",
-    "tdc_workspace_bytes", "FMT_INT8", "FMT_NVFP4",
+    "tdc_workspace_bytes", "FMT_INT8", "FMT_NVFP4", "FMT_BF16",
 ]
 
-FMT_INT8, FMT_NVFP4 = L.FMT_INT8, L.FMT_NVFP4
+FMT_INT8, FMT_NVFP4, FMT_BF16 = L.FMT_INT8, L.FMT_NVFP4, L.FMT_BF16
 
 
 def _ptr(t):
@@ -60,6 +60,12 @@ class PackedWeights:
     bias: torch.Tensor | None
     c: L.Weights = field(default=None, repr=False)
     hadamard: bool = False
+    bf16_w: torch.Tensor | None = None     # unquantised weights for the PDR BF16 fallback (R15)
+
+    def keep_bf16(self, W: torch.Tensor):
+        self.bf16_w = W.contiguous()
+        self.c.bf16_w = self.bf16_w.data_ptr()
+        return self
 
     @classmethod
     def empty(cls, n: int, k: int, device, bias: torch.Tensor | None = None):
@@ -81,7 +87,8 @@ class PackedWeights:
                    (self.fp4_codes, self.fp4_sf, self.fp4_g, self.i8_codes, self.i8_scale))
 
 
-def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamard: bool = False) -> PackedWeights:
+def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamard: bool = False,
+                      keep_bf16: bool = False) -> PackedWeights:
     """Offline pack of nn.Linear weights W [n, k] (bf16, CUDA) in both formats (P:184, R7);
     hadamard=True rotates every row by the block FHT first (R14)."""
     _check_dev(W, "W", torch.bfloat16)
@@ -94,6 +101,8 @@ def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamar
     else:
         L.check("dmpq_pack_weights", L.lib().dmpq_pack_weights(_ptr(W), n, k, ctypes.byref(pw.c), _stream(W.device)))
     pw.hadamard = hadamard
+    if keep_bf16:
+        pw.keep_bf16(W)
     return pw
 
 
@@ -125,10 +134,21 @@ class QuantAct:
             a.c = L.Act(fmt, m, k, a.codes.data_ptr(), None, None, a.row_scale.data_ptr())
         return a
 
+    @classmethod
+    def bf16(cls, X: torch.Tensor):
+        """The unquantised activation itself, for the BF16 (PDR fallback) GEMM path."""
+        _check_dev(X, "X", torch.bfloat16)
+        assert X.is_contiguous()
+        m, k = X.shape
+        a = cls(FMT_BF16, m, k, X)
+        a.c = L.Act(FMT_BF16, m, k, X.data_ptr(), None, None, None)
+        return a
+
 
 def dmpq_quantize_act(X: torch.Tensor, out_i8: QuantAct | None = None, out_fp4: QuantAct | None = None,
                       amax_out: torch.Tensor | None = None, layernorm: bool = False, ln_eps: float = 1e-6,
-                      h_out: torch.Tensor | None = None, hadamard: bool = False):
+                      h_out: torch.Tensor | None = None, hadamard: bool = False,
+                      row_abs_sum: torch.Tensor | None = None, amax_in: torch.Tensor | None = None):
     """Quantize X [m, k] (bf16, CUDA, row stride X.stride(0)) into the given outputs (Eq. 2 / P:115)."""
     _check_dev(X, "X", torch.bfloat16)
     if X.stride(1) != 1:
@@ -137,14 +157,32 @@ def dmpq_quantize_act(X: torch.Tensor, out_i8: QuantAct | None = None, out_fp4: 
     opts = None
     flags = (L.QF_LAYERNORM if layernorm else 0) | (L.QF_WRITE_H if h_out is not None else 0) | \
         (L.QF_HADAMARD if hadamard else 0)
-    if flags:
+    if flags or row_abs_sum is not None or amax_in is not None:
         opts = L.QuantOpts(flags, ln_eps, None if h_out is None else h_out.data_ptr(),
-                           0 if h_out is None else h_out.stride(0))
+                           0 if h_out is None else h_out.stride(0),
+                           None if row_abs_sum is None else row_abs_sum.data_ptr(),
+                           None if amax_in is None else amax_in.data_ptr())
     L.check("dmpq_quantize_act", L.lib().dmpq_quantize_act(
         _ptr(X), m, k, X.stride(0), None if opts is None else ctypes.byref(opts),
         None if out_i8 is None else ctypes.byref(out_i8.c), None if out_fp4 is None else ctypes.byref(out_fp4.c),
         _ptr(amax_out), _stream(X.device)))
     return out_i8, out_fp4
+
+
+def dmpq_outlier_reduce(row_sums: torch.Tensor, out: torch.Tensor):
+    """out[s] = sum_r row_sums[s, r] in FP64, fixed order (PDR statistics, R15)."""
+    seg, m = row_sums.shape
+    L.check("dmpq_outlier_reduce", L.lib().dmpq_outlier_reduce(_ptr(row_sums), m, seg, _ptr(out), _stream(row_sums.device)))
+    return out
+
+
+def dmpq_purify(fmts, ratios, prev_skipped: bool, tau_outlier: float = 25.0):
+    """Purified Cache Refresh gate (R15): BF16 if ratio > tau_outlier, INT8 after a skip."""
+    n = len(fmts)
+    f = (ctypes.c_uint8 * max(n, 1))(*fmts)
+    r = None if ratios is None else (ctypes.c_double * n)(*[float(x) for x in ratios])
+    L.lib().dmpq_purify(r, n, int(bool(prev_skipped)), float(tau_outlier), f)
+    return [int(f[i]) for i in range(n)]
 
 
 def dmpq_global_scale(amax: torch.Tensor, div: float, g_out: torch.Tensor):

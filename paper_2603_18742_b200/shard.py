@@ -2,10 +2,11 @@
 
 Each rank owns a contiguous range of token rows; weights are replicated. Every
 hot-path op is row-local, so the only communication is, once per timestep:
-  - SUM all-reduce of a zero-padded [world x blocks x 7] FP64 slot buffer (each
+  - SUM all-reduce of a zero-padded [world x blocks x 11] FP64 slot buffer (each
     rank fills only its own slot: the SUM is an exact all-gather), then a
     rank-ordered combine, so every rank holds bit-identical global statistics;
-  - MAX all-reduce of the [blocks x 4] fp32 activation amax (NVFP4 global scales).
+  - MAX all-reduce of the [blocks x 8] fp32 activation maxima (NVFP4 global scales and
+    the PDR outlier ratio's max|x|).
 Works with any torch.distributed backend (NCCL on the GPUs, gloo in the CPU tests).
 """
 from __future__ import annotations

@@ -106,3 +106,16 @@ def test_tdc_host_matches_oracle(L, orc):
             orc.tdc_update(so, cfg_o, t, do, e)
             dmpq.tdc_update(sc, cfg_c, t, dc, st)
             assert sc.e_acc == so.e_acc and sc.t_p == so.t_p
+
+
+def test_purify_matches_oracle(L, orc):
+    from paper_2603_18742_b200 import dmpq
+    rng = np.random.default_rng(3)
+    for _ in range(500):
+        fm = [int(v) for v in rng.integers(0, 2, 6)]
+        ratios = list(rng.uniform(0, 50, 6))
+        ratios[int(rng.integers(0, 6))] = 25.0
+        ps = bool(rng.integers(0, 2))
+        got = dmpq.dmpq_purify(fm, ratios, ps, 25.0)
+        assert got == [orc.purify_route(f, r, ps, 25.0) for f, r in zip(fm, ratios)]
+    assert dmpq.dmpq_purify([1, 1], None, True) == [0, 0]

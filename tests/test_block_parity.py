@@ -36,8 +36,15 @@ def close_bf16(gpu_bf16, ref64, rel=2.0 ** -7):
     assert np.linalg.norm(g - ref64) <= 4e-3 * np.linalg.norm(ref64)
 
 
-@pytest.fixture(scope="module")
-def run():
+MODES = {
+    # name: (hadamard, pdr, tau_outlier)
+    "dmpq_tdc": (False, False, 25.0),
+    "hadamard_pdr": (True, True, 9.0),   # tau_outlier between the O-input and FFN2-input ratios: mixed BF16
+}
+
+
+@pytest.fixture(scope="module", params=sorted(MODES))
+def run(request):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2603_18742_b200 import build
@@ -45,8 +52,9 @@ def run():
     build.build()
     dev = torch.device("cuda")
     M, H, F, T = 256, 128, 512, 6
+    had, pdr, tau_o = MODES[request.param]
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
-    stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008])
+    stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o)
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):
@@ -55,12 +63,14 @@ def run():
         stack.capture = cap
         d0 = stack.delta[0].clone()
         g_before = stack.g_table.clone()
+        ratio_before = None if stack.ratio[0] is None else list(stack.ratio[0])
         stack.step(x, t)
         stats = stack.end_step(t)
         rec = stack.records[-1]
         steps.append(dict(t=t, cap=cap, x=x.cpu(), delta_prev=d0.cpu(), delta_new=stack.delta[0].clone().cpu(),
                           stats=stats[0].copy(), fmts=rec.fmts[0], decision=rec.decisions[0],
-                          g=g_before.cpu(), out=stack.x_buf[0].clone().cpu()))
+                          g=g_before.cpu(), out=stack.x_buf[0].clone().cpu(), ratio=ratio_before,
+                          amax_in=stack.amax[0, 4:].cpu().numpy().copy()))
     return stack, steps
 
 
@@ -71,16 +81,19 @@ def _ln64(x):
     return (x - mu) / np.sqrt(var + 1e-6)
 
 
-def _check_quant(orc, src_bf16, act, fmt, k):
+def _check_quant(orc, src_bf16, act, fmt, k, had=False):
     from paper_2603_18742_b200 import dmpq as D
     m = src_bf16.shape[0]
+    if fmt == D.FMT_BF16:
+        return ("bf16", bits(src_bf16))
+    y = orc.fht128(orc.bf16_to_f32(bits(src_bf16)).reshape(m, k)) if had else None
     if fmt == D.FMT_NVFP4:
         g = float(act["g"].item())
-        c, s = orc.nvfp4_quantize(bits(src_bf16), g)
+        c, s = orc.nvfp4_quantize_f32(y, g) if had else orc.nvfp4_quantize(bits(src_bf16), g)
         assert np.array_equal(act["codes"].cpu().numpy(), c)
         assert np.array_equal(orc.sf_unswizzle(act["sf"].cpu().numpy(), m, k), s)
         return c, s, g
-    c, s = orc.int8_quantize(bits(src_bf16))
+    c, s = orc.int8_quantize_f32(y) if had else orc.int8_quantize(bits(src_bf16))
     assert np.array_equal(act["codes"].cpu().numpy(), c)
     assert np.array_equal(act["row_scale"].cpu().numpy(), s)
     return c, s, None
@@ -90,6 +103,8 @@ def _gemm_ref(orc, fmt, q, pw, n, k):
     """fp64/fp32 oracle output of one layer from the GPU's codes (teacher forcing)."""
     from paper_2603_18742_b200 import dmpq as D
     bias = pw.bias.cpu().numpy()
+    if fmt == D.FMT_BF16:
+        return orc.gemm_bf16(q[1], synth.bits(pw.bf16_w.cpu()), bias), False
     if fmt == D.FMT_NVFP4:
         c, s, g = q
         return orc.gemm_nvfp4(c, s, g, pw.fp4_codes.cpu().numpy(), orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k),
@@ -104,6 +119,7 @@ def test_stages_teacher_forced(run, orc):
     stack, steps = run
     W = stack.blocks[0]
     H, F = stack.H, stack.F
+    had = stack.hadamard
     n_checked = 0
     for st in steps:
         if st["fmts"] is None:
@@ -114,7 +130,7 @@ def test_stages_teacher_forced(run, orc):
         close_bf16(cap["h1"], _ln64(f32(cap["x_in"])))
         qs = {}
         for f_ in set(fm[0:3]):
-            qs[f_] = _check_quant(orc, cap["h1"], cap["a0_i8" if f_ == D.FMT_INT8 else "a0_f4"], f_, H)
+            qs[f_] = _check_quant(orc, cap["h1"], cap.get("a0_i8" if f_ == D.FMT_INT8 else "a0_f4"), f_, H, had)
         for j in range(3):
             ref, exact = _gemm_ref(orc, fm[j], qs[fm[j]], W.layers[j], H, H)
             if exact:
@@ -122,7 +138,7 @@ def test_stages_teacher_forced(run, orc):
             else:
                 close_bf16(cap[f"y{j}"], ref)
         # O projection on a = v with the gated residual
-        q1 = _check_quant(orc, cap["y2"], cap["a1"], fm[3], H)
+        q1 = _check_quant(orc, cap["y2"], cap.get("a1"), fm[3], H, had)
         yo, exact = _gemm_ref(orc, fm[3], q1, W.layers[3], H, H)
         gate = W.g1.cpu().numpy()
         xin = f32(cap["x_in"])
@@ -133,12 +149,12 @@ def test_stages_teacher_forced(run, orc):
             close_bf16(cap["x_mid"], xin + gate[None, :] * yo)
         # FFN1 (+GELU glue) and FFN2 with the gated residual
         close_bf16(cap["h2"], _ln64(f32(cap["x_mid"])))
-        q2 = _check_quant(orc, cap["h2"], cap["a2"], fm[4], H)
+        q2 = _check_quant(orc, cap["h2"], cap.get("a2"), fm[4], H, had)
         yf, _ = _gemm_ref(orc, fm[4], q2, W.layers[4], F, H)
         gelu = 0.5 * yf * (1 + np.tanh(math.sqrt(2 / math.pi) * (yf + 0.044715 * yf ** 3)))
         g_ = f32(cap["f"])
         assert np.linalg.norm(g_ - gelu) <= 1e-2 * np.linalg.norm(gelu)
-        q3 = _check_quant(orc, cap["f"], cap["a3"], fm[5], F)
+        q3 = _check_quant(orc, cap["f"], cap.get("a3"), fm[5], F, had)
         y2, exact = _gemm_ref(orc, fm[5], q3, W.layers[5], H, F)
         gate2 = W.g2.cpu().numpy()
         xmid = f32(cap["x_mid"])
@@ -151,7 +167,7 @@ def test_stages_teacher_forced(run, orc):
         dn, sref = orc.block_stats(bits(cap["x_in"]), bits(cap["x_out"]), bits(st["delta_prev"]))
         assert np.array_equal(bits(st["delta_new"]), dn)
         np.testing.assert_allclose(st["stats"][:4], sref[:4], rtol=4.2e-7)
-        np.testing.assert_allclose(st["stats"][4:], sref[4:], rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(st["stats"][4:7], sref[4:], rtol=1e-12, atol=1e-300)
     assert n_checked >= 3
 
 
@@ -188,18 +204,43 @@ def test_decisions_match_oracle(run, orc):
         if d == 0:
             gamma = None if prev_stats is None else orc.gamma_from_stats(prev_stats)
             ref = orc.route_block(gamma, stack.tau, t, prev_skipped)
+            slot_of = (0, 0, 0, 1, 2, 3)
             for j, (a, b) in enumerate(zip(ref, st["fmts"])):
+                if stack.pdr and st["ratio"] is not None:
+                    r = st["ratio"][slot_of[j]]
+                    if abs(r - stack.tau_outlier) <= 1e-6 * stack.tau_outlier:
+                        continue
+                    a = orc.purify_route(a, r, prev_skipped, stack.tau_outlier)
                 if gamma is not None and abs(gamma - stack.tau[j]) <= 1e-6 * stack.tau[j]:
                     continue
                 assert a == b, (t, j, gamma, stack.tau[j])
             mixed.update(st["fmts"])
-            e = orc.cosine_error_from_stats(st["stats"][4], st["stats"][5], st["stats"][6])
+            e = orc.cosine_error_from_stats(st["stats"][4], st["stats"][5], st["stats"][6])  # [7:] = PDR sums
             orc.tdc_update(s, cfg, t, 0, e)
             prev_stats, prev_skipped = st["stats"], False
         else:
             orc.tdc_update(s, cfg, t, 1)
             prev_stats, prev_skipped = None, True
-    assert mixed == {0, 1}, "the synthetic block should exercise both formats"
+    if stack.pdr:
+        assert 2 in mixed and mixed & {0, 1}, "the PDR mode should mix BF16 and quantized layers"
+    else:
+        assert {0, 1} <= mixed, "the synthetic block should exercise both quantized formats"
+
+
+def test_pdr_ratio_matches_oracle(run, orc):
+    """R = max|x| / mean|x| of each layer input (R15) from the GPU's statistics equals the
+    oracle's ratio of the GPU's stage inputs (h1, v, h2, f) at the last computed step."""
+    stack, steps = run
+    if not stack.pdr:
+        pytest.skip("PDR off in this mode")
+    last = [s for s in steps if s["fmts"] is not None][-1]
+    cap = last["cap"]
+    srcs = [cap["h1"], cap["y2"], cap["h2"], cap["f"]]
+    for s, src in enumerate(srcs):
+        ref = orc.outlier_ratio(bits(src))
+        got = stack.ratio[0][s]
+        assert got == pytest.approx(ref, rel=1e-5), (s, got, ref)
+        assert last["amax_in"][s] == float(np.abs(f32(src)).max())
 
 
 def test_skip_output_matches_oracle(run, orc):

@@ -256,3 +256,40 @@ def test_pack_weights_hadamard_and_gemm(D, orc, n, k):
     err_plain = np.linalg.norm(y0.cpu().numpy() - exact) / np.linalg.norm(exact)
     # transparent up to quantization (4-bit-derived weights): same error scale as the plain path
     assert err_rot < 0.25 and err_rot < 1.5 * err_plain, (err_rot, err_plain)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 32, 64), (200, 256, 1920), (257, 512, 3072)])
+def test_gemm_bf16_rel_l2(D, orc, m, n, k):
+    """BF16 fallback GEMM of the PDR gate (kind::f16): rel-L2 <= 1e-5 vs fp64."""
+    x = synth.dit_activation(m, k, seed=9 * m + k)
+    w, b = synth.linear_weight(n, k, seed=n + 11 * k)
+    pw = D.dmpq_pack_weights(w.cuda(), b, keep_bf16=True)
+    a = D.QuantAct.bf16(x.cuda())
+    y32 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y, Y32=y32)
+    torch.cuda.synchronize()
+    ref = orc.gemm_bf16(synth.bits(x), synth.bits(w), b.numpy())
+    assert rel_l2(y32.cpu().numpy(), ref) <= 1e-5
+    assert torch.equal(y.cpu(), y32.cpu().to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("m,k,had", [(300, 1920, False), (129, 3072, True), (5, 12288, False)])
+def test_pdr_statistics(D, orc, m, k, had):
+    """Per-row sum|x| (FP32, fixed order: within K * 2^-24 of the exact sum) and max|x|
+    of the layer input (exact), and the FP64 fixed-order reduction."""
+    x = synth.dit_activation(m, k, seed=m + k)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    rs = torch.zeros(1, m, dtype=torch.float32, device="cuda")
+    ain = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a8, hadamard=had, row_abs_sum=rs[0], amax_in=ain)
+    tot = torch.zeros(1, dtype=torch.float64, device="cuda")
+    D.dmpq_outlier_reduce(rs, tot)
+    torch.cuda.synchronize()
+    xf = np.abs(x.float().numpy().astype(np.float64))
+    exact = xf.sum(axis=1)
+    np.testing.assert_allclose(rs[0].cpu().numpy(), exact, rtol=k * 2.0 ** -24)
+    assert ain.item() == float(xf.max())
+    assert tot.item() == pytest.approx(float(rs[0].cpu().numpy().astype(np.float64).sum()), rel=1e-12)
+    r_gpu = ain.item() / (tot.item() / (m * k))
+    assert r_gpu == pytest.approx(orc.outlier_ratio(synth.bits(x)), rel=1e-5)

@@ -509,3 +509,43 @@ def test_pack_weights_hadamard(orc):
     what = orc.nvfp4_dequantize(pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"])
     err = np.abs(what - pk["i8_codes"] * pk["i8_scale"][:, None].astype(np.float64))
     assert np.all(err <= pk["i8_scale"][:, None] * (0.5 + 1e-5))
+
+
+# ---------------------------------------------------------------------------- Purified Cache Refresh (R15)
+
+def test_outlier_ratio_spec_examples(orc):
+    """constant magnitude -> 1; [50, 2, 2, 2] -> 50/14; one spike 1000 among
+    999 ones -> 1000 / (1999/1000); all-zero -> 1."""
+    assert orc.outlier_ratio(bf16_bits(np.full(64, -3.0, np.float32))) == 1.0
+    assert orc.outlier_ratio(bf16_bits([50.0, 2.0, 2.0, 2.0])) == pytest.approx(50.0 / 14.0, rel=1e-15)
+    x = np.ones(1000, np.float32)
+    x[17] = 1000.0
+    assert orc.outlier_ratio(bf16_bits(x)) == pytest.approx(1000.0 / (1999.0 / 1000.0), rel=1e-15)
+    assert orc.outlier_ratio(bf16_bits(np.zeros(8, np.float32))) == 1.0
+    # strided sampling (S:409): every 2nd element of [50, 9, 2, 9, 2, 9] -> [50, 2, 2]
+    assert orc.outlier_ratio(bf16_bits([50.0, 9.0, 2.0, 9.0, 2.0, 9.0]), stride=2) == pytest.approx(50.0 / 18.0)
+
+
+def test_purify_route_precedence(orc):
+    """S:420-422 and S:425: ratio exactly tau keeps the base decision (strict '>');
+    after a skip (ratio <= tau) every layer is INT8; ratio 500 -> BF16 regardless;
+    precedence outlier > post-skip > base."""
+    B, I, N = orc.FMT_BF16, orc.FMT_INT8, orc.FMT_NVFP4
+    assert orc.purify_route(N, 25.0, False, 25.0) == N
+    assert orc.purify_route(N, 24.0, True, 25.0) == I
+    assert orc.purify_route(N, 500.0, False, 25.0) == B
+    assert orc.purify_route(I, 500.0, True, 25.0) == B
+    assert orc.purify_route(N, None, False, 25.0) == N
+
+
+def test_gemm_bf16_exact_fractions(orc):
+    rng = np.random.default_rng(25)
+    x = bf16_bits(rng.standard_normal((3, 64)).astype(np.float32))
+    w = bf16_bits(rng.standard_normal((5, 64)).astype(np.float32))
+    b = rng.standard_normal(5).astype(np.float32)
+    y = orc.gemm_bf16(x, w, b)
+    xf, wf = bf16_vals(x), bf16_vals(w)
+    for i in range(3):
+        for j in range(5):
+            exact = sum(Fraction(float(xf[i, t])) * Fraction(float(wf[j, t])) for t in range(64)) + Fraction(float(b[j]))
+            assert abs(Fraction(y[i, j]) - exact) <= abs(exact) * Fraction(1, 2 ** 50) + Fraction(1, 2 ** 80)
