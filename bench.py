@@ -237,6 +237,11 @@ def run_ours(args):
     local_flops = sum(r.linear_flops for r in recs)
     gemm_t = model.gemm_time_s()
     gemm_flops = dict(model.gemm_flops)
+    brk = model.breakdown_s()
+    breakdown = {"gemm": sum(v[0] for v in gemm_t.values()) / args.steps * 1e3,
+                 "quantize": brk["quantize"] / args.steps * 1e3, "tdc": brk["tdc"] / args.steps * 1e3,
+                 "exchange": brk["exchange"] / args.steps * 1e3}
+    breakdown["host_gaps_and_other"] = elapsed / args.steps * 1e3 - sum(breakdown.values())
     model.timing = False
 
     # every rank must have taken identical TDC/routing decisions
@@ -343,6 +348,7 @@ def run_ours(args):
                    "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr,
                    "mix": mix},
         "block_step_ms": elapsed / args.steps / nb * 1e3,
+        "breakdown_ms_per_step": breakdown,
         "effective_tflops_dense_equiv": dense_flops / elapsed / 1e12,
         "wall_s_timed": wall,
         "gpu_launches": launches,

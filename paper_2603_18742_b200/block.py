@@ -136,8 +136,8 @@ class DiTStack:
         self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr)
                        for b in range(n_blocks)]
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
-        # [:, :4] amax of the quantised values (NVFP4 global scales, R3); [:, 4:] max|x| of the layer inputs (PDR)
-        self.amax = torch.zeros(n_blocks, 2 * N_SLOTS, dtype=torch.float32, device=self.device)
+        # [0] amax of the quantised values (NVFP4 global scales, R3); [1] max|x| of the layer inputs (PDR, R15)
+        self.amax = torch.zeros(2, n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
         self.row_abs = torch.zeros(n_blocks * N_SLOTS, m_local, dtype=torch.float32, device=self.device)
         self.ws = Workspace(m_local, H, F, self.device, self.g_table)
         self.delta = [torch.zeros(m_local, H, dtype=torch.bfloat16, device=self.device) for _ in range(n_blocks)]
@@ -153,6 +153,7 @@ class DiTStack:
         self.records: list[StepRecord] = []
         self.launches = 0                       # libdmpq kernel launches issued (bench's gpu_launches)
         self.timing = False                     # record CUDA events around every GEMM (roofline)
+        self.kernel_events = {"quantize": [], "tdc": [], "exchange": []}   # breakdown of the step
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
         self.capture = None                     # dict -> per-stage clones for the parity tests
@@ -172,17 +173,41 @@ class DiTStack:
             self.capture[key] = d
 
     # ------------------------------------------------------------------ one block
+    def _ev(self, kind):
+        """Context manager: CUDA events around a region when timing is on (breakdown)."""
+        stack = self
+
+        class _C:
+            def __enter__(self_):
+                if stack.timing:
+                    self_.s = torch.cuda.Event(enable_timing=True)
+                    self_.s.record()
+
+            def __exit__(self_, *a):
+                if stack.timing:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record()
+                    stack.kernel_events[kind].append((self_.s, e))
+        return _C()
+
+    def breakdown_s(self):
+        return {k: sum(s.elapsed_time(e) for s, e in v) * 1e-3 for k, v in self.kernel_events.items()}
+
     def _quant(self, b, slot, src, fmts_needed, layernorm=False, h_buf=None):
         """Quantize one activation tensor into the formats its consumers need (plus PDR
         statistics); returns {fmt: QuantAct} with FMT_BF16 -> the bf16 tensor itself."""
+        with self._ev("quantize"):
+            return self._quant_impl(b, slot, src, fmts_needed, layernorm, h_buf)
+
+    def _quant_impl(self, b, slot, src, fmts_needed, layernorm, h_buf):
         ws = self.ws
         want_h = layernorm and (D.FMT_BF16 in fmts_needed or self.capture is not None)
         a8 = ws.act(slot, D.FMT_INT8, b) if D.FMT_INT8 in fmts_needed else None
         a4 = ws.act(slot, D.FMT_NVFP4, b) if D.FMT_NVFP4 in fmts_needed else None
-        D.dmpq_quantize_act(src, out_i8=a8, out_fp4=a4, amax_out=self.amax[b, slot:slot + 1], layernorm=layernorm,
+        D.dmpq_quantize_act(src, out_i8=a8, out_fp4=a4, amax_out=self.amax[0, b, slot:slot + 1], layernorm=layernorm,
                             h_out=h_buf if want_h else None, hadamard=self.hadamard,
                             row_abs_sum=self.row_abs[b * N_SLOTS + slot] if self.pdr else None,
-                            amax_in=self.amax[b, N_SLOTS + slot:N_SLOTS + slot + 1] if self.pdr else None)
+                            amax_in=self.amax[1, b, slot:slot + 1] if self.pdr else None)
         out = {D.FMT_INT8: a8, D.FMT_NVFP4: a4}
         if D.FMT_BF16 in fmts_needed:
             out[D.FMT_BF16] = D.QuantAct.bf16(h_buf if layernorm else src)
@@ -240,6 +265,7 @@ class DiTStack:
         return out
 
     def reset_timing(self):
+        self.kernel_events = {"quantize": [], "tdc": [], "exchange": []}
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
 
@@ -255,7 +281,8 @@ class DiTStack:
             x_out = self.x_buf[b % 2]
             d = D.tdc_decide(self.tdc[b], self.cfg, t) if self.tdc_enabled else L.TDC_COMPUTE
             if d == L.TDC_DECIDE_SKIP:
-                D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
+                with self._ev("tdc"):
+                    D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
                 self.launches += 1
                 rec.fmts.append(None)
                 rec.gammas.append(float("nan"))
@@ -268,8 +295,9 @@ class DiTStack:
                         fmts = D.dmpq_purify(fmts, [self.ratio[b][s] for s in SLOT_OF_LAYER], self.prev_skipped[b],
                                              self.tau_outlier)
                 rec.linear_flops += self._compute_block(b, x_in, x_out, fmts)
-                D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
-                           self.ws.tdc_ws)
+                with self._ev("tdc"):
+                    D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
+                               self.ws.tdc_ws)
                 self.launches += 1
                 rec.fmts.append(fmts)
                 rec.gammas.append(gamma)
@@ -282,16 +310,21 @@ class DiTStack:
         """Per-step exchange + host decisions: combine the statistics of all ranks
         (slot-packed SUM all-reduce = exact all-gather; MAX all-reduce for amax), copy
         them to the host once, update TDC (Eq. 10) and the NVFP4 global scales (R3)."""
-        if self.pdr:   # per-slot sum|x| of this rank's rows -> its stats slot (FP64, fixed order)
-            D.dmpq_outlier_reduce(self.row_abs, self.pdr_sums)
-            self.stats_slots[self.rank, :, L.STATS_LEN:] = self.pdr_sums.view(self.nb, N_SLOTS)
+        with self._ev("exchange"):
+            if self.pdr:   # per-slot sum|x| of this rank's rows -> its stats slot (FP64, fixed order)
+                D.dmpq_outlier_reduce(self.row_abs, self.pdr_sums)
+                self.stats_slots[self.rank, :, L.STATS_LEN:] = self.pdr_sums.view(self.nb, N_SLOTS)
+                self.launches += 1
+            if self.group is not None and self.world > 1:
+                torch.distributed.all_reduce(self.stats_slots, op=torch.distributed.ReduceOp.SUM, group=self.group)
+                torch.distributed.all_reduce(self.amax, op=torch.distributed.ReduceOp.MAX, group=self.group)
+            # next step's NVFP4 global scales from the (all-rank) amax of this step (R3)
+            D.dmpq_global_scale(self.amax[0].view(-1), 1344.0, self.g_table.view(-1))
             self.launches += 1
-        # one exchange per step; the D2H copy inside synchronises the stream
-        stats = exchange(self.stats_slots, self.amax, self.group, self.world)
-        D.dmpq_global_scale(self.amax[:, :N_SLOTS].contiguous().view(-1), 1344.0, self.g_table.view(-1))
-        self.launches += 1
+        # the D2H copy inside synchronises the stream (one exchange per step)
+        stats = exchange(self.stats_slots, self.amax, None, 1)
         if self.pdr:
-            amax_in = self.amax[:, N_SLOTS:].cpu().numpy().astype(np.float64)
+            amax_in = self.amax[1].cpu().numpy().astype(np.float64)
         rec = self.records[-1]
         for b in range(self.nb):
             d = rec.decisions[b]

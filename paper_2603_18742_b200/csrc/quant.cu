@@ -101,40 +101,34 @@ __device__ __forceinline__ uint32_t int8x4(f2 q01, f2 q23) {
     return r;
 }
 
-// FHT over the 128-element block held by this thread (64 elements) and its partner lane
-// (tid ^ 1): stages h = 1..32 in-thread (packed), h = 64 across the pair, then * fl32(1/sqrt(128)).
-// Every butterfly is one FP32 add/sub in the oracle's order (bit-exact, R14).
-__device__ __forceinline__ void fht128_chunk(float (&y)[64], bool upper) {
-    // h = 1: pairs (e, e+1), e even; pack two pairs per instruction
+// FHT over the 128-element block held by this thread (64 elements as 32 packed pairs
+// Y[p] = (y[2p], y[2p+1])) and its partner lane (tid ^ 1): stage h = 1 within each pair
+// (scalar add/sub), stages h = 2..32 between pairs p and p + h/2 (packed FADD2, no register
+// moves), h = 64 across the lane pair (two shuffles + one exact FFMA2 per pair), then
+// * fl32(1/sqrt(128)). Every butterfly is one FP32 add/sub in the oracle's order (R14).
+__device__ __forceinline__ void fht128_chunk(f2 (&Y)[32], bool upper) {
 #pragma unroll
-    for (int e = 0; e < 64; e += 4) {
-        const f2 a = f2make(y[e], y[e + 2]), b = f2make(y[e + 1], y[e + 3]);
-        const f2 s = add2(a, b), d = add2(a, f2make(-y[e + 1], -y[e + 3]));
-        y[e] = f2lo(s); y[e + 2] = f2hi(s); y[e + 1] = f2lo(d); y[e + 3] = f2hi(d);
+    for (int p = 0; p < 32; ++p) {
+        const float a = f2lo(Y[p]), b = f2hi(Y[p]);
+        Y[p] = f2make(__fadd_rn(a, b), __fsub_rn(a, b));
     }
 #pragma unroll
-    for (int h = 2; h < 64; h <<= 1) {
+    for (int hp = 1; hp < 32; hp <<= 1) {            // pair stride hp = h/2, h = 2..32
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-            if (e & h) continue;
-            const f2 a = f2make(y[e], y[e + 1]), b = f2make(y[e + h], y[e + h + 1]);
-            const f2 s = add2(a, b), d = add2(a, f2make(-y[e + h], -y[e + h + 1]));
-            y[e] = f2lo(s); y[e + 1] = f2hi(s); y[e + h] = f2lo(d); y[e + h + 1] = f2hi(d);
+        for (int p = 0; p < 32; ++p) {
+            if (p & hp) continue;
+            const f2 a = Y[p], b = Y[p + hp];
+            Y[p] = add2(a, b);
+            Y[p + hp] = sub2(a, b);
         }
     }
     // h = 64: lower lane keeps a + b, upper lane gets a - b = fma(-1, b, a) (exact product, one rounding)
     const f2 sg = upper ? f2make(-1.0f, -1.0f) : f2make(1.0f, 1.0f);
-#pragma unroll
-    for (int e = 0; e < 64; e += 2) {
-        const float o0 = __shfl_xor_sync(0xffffffffu, y[e], 1), o1 = __shfl_xor_sync(0xffffffffu, y[e + 1], 1);
-        const f2 r = fma2(sg, f2make(y[e], y[e + 1]), f2make(o0, o1));
-        y[e] = f2lo(r); y[e + 1] = f2hi(r);
-    }
     const f2 sc = f2make(0.08838834764831845f, 0.08838834764831845f);   // fl32(1/sqrt(128))
 #pragma unroll
-    for (int e = 0; e < 64; e += 2) {
-        const f2 r = mul2(f2make(y[e], y[e + 1]), sc);
-        y[e] = f2lo(r); y[e + 1] = f2hi(r);
+    for (int p = 0; p < 32; ++p) {
+        const float o0 = __shfl_xor_sync(0xffffffffu, f2lo(Y[p]), 1), o1 = __shfl_xor_sync(0xffffffffu, f2hi(Y[p]), 1);
+        Y[p] = mul2(fma2(sg, Y[p], f2make(o0, o1)), sc);
     }
 }
 
@@ -150,7 +144,20 @@ __device__ __forceinline__ void load_chunks(uint4 (&v)[NC][8], const uint16_t* x
     }
 }
 
-template <int NC, bool HAD>
+// Coalesced row load for the chunk layout: the group's threads read 16-byte vectors
+// consecutively (lane-contiguous), park them in shared memory (one 16-byte pad per
+// 128-byte chunk keeps the later chunk reads at the 4-wavefront minimum), and each
+// thread then picks up its own 64-element chunk.
+template <int VPT>
+__device__ __forceinline__ void load_row_coalesced(uint4 (&pv)[VPT], const uint16_t* xr, int tid, int tpr, int nvec, bool valid) {
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int vi = tid + j * tpr;
+        pv[j] = (valid && vi < nvec) ? ldg_stream(xr + (size_t)vi * 8) : make_uint4(0, 0, 0, 0);
+    }
+}
+
+template <int NC, bool HAD, bool SMEM>
 __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams p, int tpr) {
     __shared__ float red[8 * 8 * 8];
     const int lane = threadIdx.x & 31;
@@ -165,13 +172,50 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
     float my_amax = 0.0f, my_amax_in = 0.0f;
     int parity = 0;
 
-    int row = blockIdx.x * groups + group;
-    uint4 v[NC][8];
-    load_chunks<NC>(v, p.X + (size_t)row * p.ldx, tid, tpr, nch, row < p.m);
-    while (row < p.m) {
+    // Every group of the CTA runs the same number of iterations (rows past m are computed on
+    // zeros and not stored), so the shuffles and named barriers below are provably convergent
+    // (no WARPSYNC/collective fallback code around the FHT's lane exchange).
+    const int first = blockIdx.x * groups;
+    const int iters = first < p.m ? (p.m - first + stride - 1) / stride : 0;
+    int row = first + group;
+    // SMEM: coalesced loads transposed through shared memory (long rows); otherwise each thread
+    // reads its own 128-byte chunk directly (fewer registers; better for short rows).
+    constexpr int VPT = SMEM ? 8 * NC : 1;
+    const int nvec = p.k >> 3;
+    extern __shared__ uint4 qsm[];                  // [groups][nch][9] (8 vectors + 1 pad per chunk)
+    uint4* gbuf = qsm + (size_t)group * nch * 9;
+    uint4 pv[VPT];
+    uint4 dv[SMEM ? 1 : NC][SMEM ? 1 : 8];
+    if constexpr (SMEM) load_row_coalesced<VPT>(pv, p.X + (size_t)row * p.ldx, tid, tpr, nvec, row < p.m);
+    else load_chunks<NC>(dv, p.X + (size_t)row * p.ldx, tid, tpr, nch, row < p.m);
+    for (int it = 0; it < iters; ++it) {
+        const bool live = row < p.m;
         const int next = row + stride;
-        uint4 nv[NC][8];   // prefetch the next row while this one is processed
-        load_chunks<NC>(nv, p.X + (size_t)next * p.ldx, tid, tpr, nch, next < p.m);
+        uint4 v[NC][8];
+        if constexpr (SMEM) {
+            // transpose through smem: lane-contiguous vectors -> per-thread 64-element chunks
+            GroupReduce::named_barrier(1 + group, tpr);     // previous row's chunk reads are done
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const int vi = tid + j * tpr;
+                if (vi < nvec) gbuf[(vi >> 3) * 9 + (vi & 7)] = pv[j];
+            }
+            GroupReduce::named_barrier(1 + group, tpr);
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const int c = tid + i * tpr;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[i][j] = (c < nch) ? gbuf[c * 9 + j] : make_uint4(0, 0, 0, 0);
+            }
+            // prefetch the next row while this one is processed
+            load_row_coalesced<VPT>(pv, p.X + (size_t)next * p.ldx, tid, tpr, nvec, next < p.m);
+        } else {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[i][j] = dv[i][j];
+            load_chunks<NC>(dv, p.X + (size_t)next * p.ldx, tid, tpr, nch, next < p.m);
+        }
         const int a0 = parity * 4;
         if (p.flags & DMPQ_QF_LAYERNORM) {
             // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue, R13)
@@ -211,7 +255,7 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
 #pragma unroll
                     for (int t = 0; t < 4; ++t) w[t] = pack_bf16x2_f2(mul2(add2(bf16x2_to_f2(w[t]), nm), rs));
                     v[i][j] = (c < nch) ? make_uint4(w[0], w[1], w[2], w[3]) : make_uint4(0, 0, 0, 0);
-                    if ((p.flags & DMPQ_QF_WRITE_H) && c < nch)
+                    if ((p.flags & DMPQ_QF_WRITE_H) && c < nch && live)
                         *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)c * 64 + j * 8) = v[i][j];
                 }
             }
@@ -232,12 +276,12 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
                 }
             my_amax_in = fmaxf(my_amax_in, mx);
             const float rs = gr.sum(sa, a0 + 3);
-            if (tid == 0 && p.row_abs_sum) p.row_abs_sum[row] = rs;
+            if (tid == 0 && p.row_abs_sum && live) p.row_abs_sum[row] = rs;
         }
         // per-16-block |x| maxima (4 per chunk) and this thread's row maximum
         float bmax[NC][4];
         float tmax = 0.0f;
-        float y[HAD ? NC : 1][HAD ? 64 : 1];
+        f2 Y[HAD ? NC : 1][HAD ? 32 : 1];
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
             const bool ok = tid + i * tpr < nch;
@@ -246,14 +290,14 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
                 for (int j = 0; j < 8; ++j) {
                     const uint32_t w[4] = {v[i][j].x, v[i][j].y, v[i][j].z, v[i][j].w};
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) { y[i][8 * j + 2 * t] = bf16lo(w[t]); y[i][8 * j + 2 * t + 1] = bf16hi(w[t]); }
+                    for (int t = 0; t < 4; ++t) Y[i][4 * j + t] = bf16x2_to_f2(w[t]);
                 }
-                fht128_chunk(y[i], (tid & 1) != 0);
+                fht128_chunk(Y[i], (tid & 1) != 0);
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
                     float mx = 0.0f;
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) mx = fmaxf(mx, fabsf(y[i][16 * b + e]));
+                    for (int e = 0; e < 8; ++e) mx = fmaxf(mx, fmaxf(fabsf(f2lo(Y[i][8 * b + e])), fabsf(f2hi(Y[i][8 * b + e]))));
                     bmax[i][b] = ok ? mx : 0.0f;
                 }
             } else {
@@ -268,7 +312,7 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
         }
         my_amax = fmaxf(my_amax, tmax);
 
-        if (want_fp4) {
+        if (want_fp4 && live) {
             uint8_t* sf_row = p.fp4_sf + (size_t)(row >> 7) * p.kc4 * 512 + (row & 31) * 16 + ((row & 127) >> 5) * 4;
 #pragma unroll
             for (int i = 0; i < NC; ++i) {
@@ -288,7 +332,7 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
                         for (int u = 0; u < 4; ++u) {
                             const int e = 16 * b + 8 * t + 2 * u;
                             f2 q;
-                            if constexpr (HAD) q = mul2(f2make(y[i][e], y[i][e + 1]), r2);
+                            if constexpr (HAD) q = mul2(Y[i][e >> 1], r2);
                             else {
                                 const uint4& vv = v[i][e >> 3];
                                 const uint32_t ww = ((e & 7) == 0) ? vv.x : ((e & 7) == 2) ? vv.y : ((e & 7) == 4) ? vv.z : vv.w;
@@ -308,12 +352,12 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
         if (want_i8) {
             const float a = gr.max(tmax, a0 + 2);
             const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
-            if (tid == 0) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+            if (tid == 0 && live) p.i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
             const f2 r2 = f2make(rcp, rcp);
 #pragma unroll
             for (int i = 0; i < NC; ++i) {
                 const int c = tid + i * tpr;
-                if (c >= nch) continue;
+                if (c >= nch || !live) continue;
                 uint4* op = reinterpret_cast<uint4*>(p.i8_codes + (size_t)row * p.k + (size_t)c * 64);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {   // 16 elements -> one 16-byte store
@@ -323,8 +367,8 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
                         const int e = 16 * j + 4 * t;
                         f2 q0, q1;
                         if constexpr (HAD) {
-                            q0 = mul2(f2make(y[i][e], y[i][e + 1]), r2);
-                            q1 = mul2(f2make(y[i][e + 2], y[i][e + 3]), r2);
+                            q0 = mul2(Y[i][e >> 1], r2);
+                            q1 = mul2(Y[i][(e >> 1) + 1], r2);
                         } else {
                             const uint4& vv = v[i][e >> 3];
                             const uint32_t w0 = ((e & 7) == 0) ? vv.x : vv.z, w1 = ((e & 7) == 0) ? vv.y : vv.w;
@@ -337,10 +381,6 @@ __global__ void __launch_bounds__(256) quant_act_chunk_kernel(const QuantParams 
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < NC; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[i][j] = nv[i][j];
         row = next;
         parity ^= 1;
     }
@@ -605,7 +645,7 @@ __global__ void global_scale_kernel(const float* amax, float div, float* g_out, 
     }
 }
 
-template <int NC>
+template <int NC, bool SMEM>
 static void launch_quant_had(const QuantParams& p, int tpr, cudaStream_t s) {
     const int groups = (256 % tpr == 0) ? 256 / tpr : 1;
     const int threads = groups * tpr;
@@ -613,7 +653,8 @@ static void launch_quant_had(const QuantParams& p, int tpr, cudaStream_t s) {
     int grid = num_sms() * (2048 / threads);
     if (grid > ctas_needed) grid = ctas_needed;
     if (grid < 1) grid = 1;
-    quant_act_chunk_kernel<NC, true><<<grid, threads, 0, s>>>(p, tpr);
+    const int smem = SMEM ? groups * (p.k / 64) * 9 * 16 : 0;
+    quant_act_chunk_kernel<NC, true, SMEM><<<grid, threads, smem, s>>>(p, tpr);
 }
 
 template <int NV, bool WR>
@@ -679,7 +720,8 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
         // chunk layout: 64 elements per thread, FHT stages 1..32 in-thread
         const int nch = k / 64;
         const int tpr = (nch + 31) / 32 * 32;
-        launch_quant_had<1>(p, tpr, st);
+        if (k > 4096) launch_quant_had<1, true>(p, tpr, st);   // long rows: coalesced + smem transpose
+        else launch_quant_had<1, false>(p, tpr, st);
         return check_launch("dmpq_quantize_act");
     }
     const int nvec = k / 8;

@@ -70,7 +70,7 @@ def run(request):
         steps.append(dict(t=t, cap=cap, x=x.cpu(), delta_prev=d0.cpu(), delta_new=stack.delta[0].clone().cpu(),
                           stats=stats[0].copy(), fmts=rec.fmts[0], decision=rec.decisions[0],
                           g=g_before.cpu(), out=stack.x_buf[0].clone().cpu(), ratio=ratio_before,
-                          amax_in=stack.amax[0, 4:].cpu().numpy().copy()))
+                          amax_in=stack.amax[1, 0].cpu().numpy().copy()))
     return stack, steps
 
 
