@@ -202,16 +202,28 @@ def run_ours(args):
         if group is not None:
             torch.distributed.barrier(group=group)
 
-    # ---- warm-up (untimed): TDC warm-up steps and kernel/JIT-free first launches
-    for t in range(args.warmup):
-        model.step(steps_inputs[t], t)
-        model.end_step(t)
-    torch.cuda.synchronize()
-    barrier()
+    def allmax_sum(vals):
+        """(max over ranks of vals[0], sum over ranks of vals[1])"""
+        tt = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if group is None:
+            return float(tt[0]), float(tt[1])
+        mx, sm = tt.clone(), tt.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX, group=group)
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM, group=group)
+        return float(mx[0]), float(sm[1])
 
-    # ---- timed: K steps, device-resident inputs
-    model.timing = True
-    model.reset_timing()
+    def warmup():
+        """W untimed steps from a fresh state (TDC warm-up, graph capture, first launches)."""
+        model.reset_state()
+        for t in range(args.warmup):
+            model.step(steps_inputs[t], t)
+            model.end_step(t)
+        torch.cuda.synchronize()
+        barrier()
+
+    # ---- pass A (headline): K timed steps, device-resident inputs, CUDA graphs per block pattern
+    model.use_graphs = not args.no_graphs
+    warmup()
     launches0 = model.launches
     rec0 = len(model.records)
     clocks = ClockSampler(local)
@@ -222,9 +234,12 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall0 = time.perf_counter()
     ev0.record()
+    host_issue = 0.0
     for i in range(args.steps):
         t = args.warmup + i
-        model.step(steps_inputs[t], t)
+        h0 = time.perf_counter()
+        model.step(steps_inputs[t], t)      # enqueues the step (no synchronisation)
+        host_issue += time.perf_counter() - h0
         model.end_step(t)
     ev1.record()
     torch.cuda.synchronize()
@@ -235,14 +250,7 @@ def run_ours(args):
     launches = model.launches - launches0
     recs = model.records[rec0:]
     local_flops = sum(r.linear_flops for r in recs)
-    gemm_t = model.gemm_time_s()
-    gemm_flops = dict(model.gemm_flops)
-    brk = model.breakdown_s()
-    breakdown = {"gemm": sum(v[0] for v in gemm_t.values()) / args.steps * 1e3,
-                 "quantize": brk["quantize"] / args.steps * 1e3, "tdc": brk["tdc"] / args.steps * 1e3,
-                 "exchange": brk["exchange"] / args.steps * 1e3}
-    breakdown["host_gaps_and_other"] = elapsed / args.steps * 1e3 - sum(breakdown.values())
-    model.timing = False
+    mix = model.mix(recs)
 
     # every rank must have taken identical TDC/routing decisions
     sig = float(sum((i + 1) * (2 + d + sum(f or [])) for r in recs for i, (d, f) in enumerate(zip(r.decisions, r.fmts))))
@@ -250,58 +258,56 @@ def run_ours(args):
         s = torch.tensor([sig, -sig], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(s, op=torch.distributed.ReduceOp.MAX, group=group)
         assert float(s[0]) == sig and float(s[1]) == -sig, "ranks disagree on the per-step decisions"
-
-    tt = torch.tensor([elapsed, local_flops], dtype=torch.float64, device=dev)
-    if group is not None:
-        mx = tt.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX, group=group)
-        sm = tt.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM, group=group)
-        elapsed, total_flops = float(mx[0]), float(sm[1])
-    else:
-        total_flops = local_flops
+    elapsed, total_flops = allmax_sum([elapsed, local_flops])
     value = total_flops / elapsed / 1e12
-    mix = model.mix(recs)
     dense_flops = 2.0 * M * (4 * H * H + 2 * H * F) * nb * args.steps
 
-    # ---- e2e: the same steps through host buffers (pinned H2D of the step input, D2H of the output)
+    # ---- pass B: the same timesteps again, launched eagerly with CUDA events around every
+    # GEMM and every quantize / TDC kernel on the launching stream (roofline + breakdown)
+    model.use_graphs = False
+    warmup()
+    model.timing = True
+    model.reset_timing()
+    eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eb0.record()
+    for i in range(args.steps):
+        t = args.warmup + i
+        model.step(steps_inputs[t], t)
+        model.end_step(t)
+    eb1.record()
+    torch.cuda.synchronize()
+    model.timing = False
+    elapsed_b = eb0.elapsed_time(eb1) * 1e-3
+    gemm_t = model.gemm_time_s()
+    gemm_flops = dict(model.gemm_flops)
+    brk = model.breakdown_s()
+    breakdown = {"gemm": sum(v[0] for v in gemm_t.values()) / args.steps * 1e3,
+                 "quantize": brk["quantize"] / args.steps * 1e3, "tdc": brk["tdc"] / args.steps * 1e3,
+                 "exchange": brk["exchange"] / args.steps * 1e3}
+    breakdown["host_gaps_and_other"] = elapsed_b / args.steps * 1e3 - sum(breakdown.values())
+    breakdown["pass"] = "eager replay of the timed steps with per-launch CUDA events"
+
+    # ---- pass C (e2e): the same steps through host buffers (pinned H2D of each step's input,
+    # D2H of its output), graphs as in pass A
     host_in = {t: steps_inputs[t].cpu().pin_memory() for t in steps_inputs}
     host_out = torch.empty(m, H, dtype=torch.bfloat16).pin_memory()
-    # replay the timed steps' trajectory positions from a fresh TDC state so decisions match
-    e2e_model_state = None
-    model2 = model
-    model2.records = model2.records[:rec0]
-    # restore TDC/routing state to the start of the timed region by re-running the warm-up
-    for b in range(nb):
-        model2.tdc[b] = D.tdc_new_state()
-        model2.prev_stats[b] = None
-        model2.prev_skipped[b] = False
-    for t in range(args.warmup):
-        model2.step(steps_inputs[t], t)
-        model2.end_step(t)
-    flops2_0 = sum(r.linear_flops for r in model2.records)
-    dev_in = torch.empty(m, H, dtype=torch.bfloat16, device=dev)
-    torch.cuda.synchronize()
-    barrier()
+    model.use_graphs = not args.no_graphs
+    warmup()
+    flops2_0 = sum(r.linear_flops for r in model.records)
+    dev_in = model.x_in0 if model.use_graphs else torch.empty(m, H, dtype=torch.bfloat16, device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
         t = args.warmup + i
         dev_in.copy_(host_in[t], non_blocking=True)
-        out = model2.step(dev_in, t)
-        model2.end_step(t)
+        out = model.step(dev_in, t)
+        model.end_step(t)
         host_out.copy_(out, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
     e2e_t = e0.elapsed_time(e1) * 1e-3
-    e2e_flops = sum(r.linear_flops for r in model2.records) - flops2_0
-    et = torch.tensor([e2e_t, e2e_flops], dtype=torch.float64, device=dev)
-    if group is not None:
-        mx = et.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX, group=group)
-        sm = et.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM, group=group)
-        e2e_t, e2e_flops = float(mx[0]), float(sm[1])
+    e2e_flops = sum(r.linear_flops for r in model.records) - flops2_0
+    e2e_t, e2e_flops = allmax_sum([e2e_t, e2e_flops])
     e2e_val = e2e_flops / e2e_t / 1e12
 
     if rank != 0:
@@ -317,7 +323,7 @@ def run_ours(args):
         if n:
             ach = gemm_flops[f] / secs / 1e12
             by_fmt[name] = {"achieved": ach, "peak": sus * ratio, "frac": ach / (sus * ratio), "launches": n,
-                            "avg_launch_us": secs / n * 1e6, "time_share_of_step": secs / elapsed}
+                            "avg_launch_us": secs / n * 1e6, "time_share_of_step": secs / elapsed_b}
     dom = max(by_fmt, key=lambda k: by_fmt[k]["time_share_of_step"]) if by_fmt else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -330,7 +336,8 @@ def run_ours(args):
                     "unit": "TFLOP/s", "frac": d["frac"], "traffic": traffic,
                     "peak_source": f"{peak_kind} bf16 sustained {sus} TF/s x {dict(nvfp4=4, int8=2, bf16=1)[dom]} "
                                    f"(nominal {dom}:bf16 ratio)",
-                    "by_format": by_fmt}
+                    "by_format": by_fmt,
+                    "timing": "CUDA events around every GEMM launch on its stream, eager replay of the timed steps"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -345,12 +352,14 @@ def run_ours(args):
         "config": {"workload": desc, "blocks": nb, "hidden": H, "ffn": F, "tokens_total": M, "tokens_per_rank": m,
                    "timesteps": list(range(args.warmup, args.warmup + args.steps)), "T": T,
                    "parallelism": f"token-shard x{world}", "l2": "inputs larger than L2 (multi-GB working set per step)",
+                   "cuda_graphs": not args.no_graphs,
                    "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr,
                    "mix": mix},
         "block_step_ms": elapsed / args.steps / nb * 1e3,
         "breakdown_ms_per_step": breakdown,
         "effective_tflops_dense_equiv": dense_flops / elapsed / 1e12,
         "wall_s_timed": wall,
+        "host_issue_ms_per_step": host_issue / args.steps * 1e3,
         "gpu_launches": launches,
         "clocks": clk,
         "roofline": roofline,
@@ -373,6 +382,7 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override the block count (development only)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="launch every kernel eagerly (no CUDA graphs)")
     ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
     ap.add_argument("--pdr", action="store_true", help="enable the Purified Cache Refresh outlier gate (P:241, "
                     "NEXT-3; off by default: the north_star path is DMPQ + TDC)")

@@ -55,6 +55,11 @@ typedef enum { DMPQ_FMT_INT8 = 0, DMPQ_FMT_NVFP4 = 1, DMPQ_FMT_BF16 = 2 } dmpq_f
 const char* dmpq_last_error(void);
 const char* dmpq_version(void);
 
+/* Set the per-kernel launch attributes (dynamic shared memory) on the current device
+ * ahead of time, so that later calls may be captured into CUDA graphs. Optional:
+ * every call sets what it needs on first use. */
+dmpq_status dmpq_prepare(void);
+
 /* ========================================================================== */
 /* Sizing helpers                                                             */
 /* ========================================================================== */

@@ -71,6 +71,7 @@ class TdcConfig(ctypes.Structure):
 _SIGNATURES = {
     "dmpq_last_error": ([], ctypes.c_char_p),
     "dmpq_version": ([], ctypes.c_char_p),
+    "dmpq_prepare": ([], c_int),
     "dmpq_sf_bytes": ([c_int, c_int], c_size_t),
     "tdc_workspace_bytes": ([c_int, c_int], c_size_t),
     "dmpq_pack_weights": ([c_void_p, c_int, c_int, ctypes.POINTER(Weights), c_void_p], c_int),

@@ -157,6 +157,12 @@ class DiTStack:
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
         self.capture = None                     # dict -> per-stage clones for the parity tests
+        # CUDA graphs: one per (block, decision, formats) pattern, captured on first use and
+        # replayed afterwards (pointers are static per block; the step input is copied into x_in0)
+        self.use_graphs = False
+        self.graphs = [dict() for _ in range(n_blocks)]
+        self.graph_pool = None
+        self.x_in0 = torch.empty(m_local, H, dtype=torch.bfloat16, device=self.device)
         self.pdr_sums = torch.zeros(n_blocks * N_SLOTS, dtype=torch.float64, device=self.device)
 
     def _cap(self, key, t):
@@ -243,7 +249,6 @@ class DiTStack:
             self._cap_act("a3", q3[fmts[5]])
         self._gemm(q3[fmts[5]], W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
         self._cap("x_out", x_out)
-        self.launches += 4 + 6
         return 2.0 * m * (4 * H * H + 2 * H * F)
 
     def _gemm(self, a, w, **kw):
@@ -270,37 +275,76 @@ class DiTStack:
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
 
     # ------------------------------------------------------------------ one timestep
+    def reset_state(self):
+        """Back to t = 0: TDC states, routing history, caches, global scales."""
+        for bi in range(self.nb):
+            self.tdc[bi] = D.tdc_new_state()
+            self.prev_stats[bi] = None
+            self.prev_skipped[bi] = False
+            self.ratio[bi] = None
+            self.delta[bi].zero_()
+        self.g_table.fill_(1.0)
+        self.records = []
+
+    def _block_work(self, b, x_in, x_out, d, fmts):
+        """Enqueue one block's kernels (capturable: no host sync, no allocation)."""
+        if d == L.TDC_DECIDE_SKIP:
+            with self._ev("tdc"):
+                D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
+            return 0.0
+        flops = self._compute_block(b, x_in, x_out, fmts)
+        with self._ev("tdc"):
+            D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
+                       self.ws.tdc_ws)
+        return flops
+
     def step(self, x0: torch.Tensor, t: int) -> torch.Tensor:
         """Run all blocks at timestep t on this rank's rows; returns the last output
         (a view of an internal buffer). Call end_step(t) afterwards."""
         rec = StepRecord(t)
         self.amax.zero_()
         self.stats_slots.zero_()
+        graphs = self.use_graphs and not self.timing and self.capture is None
+        if graphs and x0.data_ptr() != self.x_in0.data_ptr():
+            self.x_in0.copy_(x0)
+            x0 = self.x_in0
         x_in = x0
         for b in range(self.nb):
             x_out = self.x_buf[b % 2]
             d = D.tdc_decide(self.tdc[b], self.cfg, t) if self.tdc_enabled else L.TDC_COMPUTE
-            if d == L.TDC_DECIDE_SKIP:
-                with self._ev("tdc"):
-                    D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
-                self.launches += 1
-                rec.fmts.append(None)
-                rec.gammas.append(float("nan"))
-            else:
+            fmts, gamma = None, float("nan")
+            if d != L.TDC_DECIDE_SKIP:
                 if self.force_fmt is not None:
-                    fmts, gamma = [self.force_fmt] * 6, float("nan")
+                    fmts = [self.force_fmt] * 6
                 else:
                     fmts, gamma, _ = D.dmpq_predict(self.prev_stats[b], self.tau, t, self.prev_skipped[b])
                     if self.pdr and self.ratio[b] is not None:
                         fmts = D.dmpq_purify(fmts, [self.ratio[b][s] for s in SLOT_OF_LAYER], self.prev_skipped[b],
                                              self.tau_outlier)
-                rec.linear_flops += self._compute_block(b, x_in, x_out, fmts)
-                with self._ev("tdc"):
-                    D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
-                               self.ws.tdc_ws)
-                self.launches += 1
-                rec.fmts.append(fmts)
-                rec.gammas.append(gamma)
+            if graphs:
+                key = (d, None if fmts is None else tuple(fmts))
+                g = self.graphs[b].get(key)
+                if g is None:
+                    # capture on a side stream without a device-wide sync (torch.cuda.graph's
+                    # context manager synchronises; this runs mid-step on first use of a pattern)
+                    if self.graph_pool is None:
+                        L.check("dmpq_prepare", L.lib().dmpq_prepare())
+                        self.graph_pool = torch.cuda.graph_pool_handle()
+                        self.capture_stream = torch.cuda.Stream(device=self.device)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.stream(self.capture_stream):
+                        g.capture_begin(pool=self.graph_pool)
+                        self._block_work(b, x_in, x_out, d, fmts)
+                        g.capture_end()
+                    self.graphs[b][key] = g
+                g.replay()
+                flops = 0.0 if d == L.TDC_DECIDE_SKIP else 2.0 * self.m * (4 * self.H * self.H + 2 * self.H * self.F)
+            else:
+                flops = self._block_work(b, x_in, x_out, d, fmts)
+            self.launches += 1 if d == L.TDC_DECIDE_SKIP else 11
+            rec.linear_flops += flops
+            rec.fmts.append(None if d == L.TDC_DECIDE_SKIP else fmts)
+            rec.gammas.append(gamma)
             rec.decisions.append(d)
             x_in = x_out
         self.records.append(rec)

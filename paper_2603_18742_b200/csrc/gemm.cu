@@ -431,6 +431,15 @@ static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, i
 }
 
 template <int KIND, int BN, int STAGES>
+static dmpq_status set_pair_attrs() {
+    using L = PairLayout<KIND, BN, STAGES>;
+    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             L::TOTAL) != cudaSuccess)
+        return check_launch("dmpq_gemm(smem attribute)");
+    return DMPQ_OK;
+}
+
+template <int KIND, int BN, int STAGES>
 static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
     using L = PairLayout<KIND, BN, STAGES>;
     constexpr bool FP4 = KIND == 1;
@@ -451,10 +460,10 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     p.num_n_tiles = (p.n + BN - 1) / BN;
     p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
     auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES>;
-    static bool attr_set = false;
+    static bool attr_set = false;   // per process and kernel (dmpq_prepare sets them ahead of graph capture)
     if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
-            return check_launch("dmpq_gemm(smem attribute)");
+        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES>();
+        if (rc != DMPQ_OK) return rc;
         attr_set = true;
     }
     const int tiles = p.num_m_tiles * p.num_n_tiles;
@@ -467,6 +476,14 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
 }  // namespace dmpq
 
 using namespace dmpq;
+
+extern "C" dmpq_status dmpq_prepare(void) {
+    DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_prepare: needs an sm_100 device");
+    dmpq_status rc = set_pair_attrs<0, 256, 6>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 6>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
+    return rc;
+}
 
 extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const dmpq_epilogue* ep, uint16_t* Y, int ldy,
                                  float* Y32, int32_t* acc_or_null, dmpq_stream_t s) {
