@@ -67,6 +67,8 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8
 // mainloop of tile i+1). Epilogue: TMEM -> registers -> 64B-swizzled smem staging
 // -> TMA store; per-column vectors (bias, w_scale, gate) staged in smem per tile.
 // ============================================================================
+constexpr int EPI_WARPS = 8;   // epilogue warps per CTA (2 per TMEM lane quarter, column-interleaved)
+
 template <int KIND, int BN, int STAGES>   // KIND: 0 INT8, 1 NVFP4, 2 BF16
 struct PairLayout {
     static constexpr bool FP4 = KIND == 1;
@@ -77,7 +79,7 @@ struct PairLayout {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
     static constexpr int PAIR_TX = 2 * STAGE_BYTES;               // bytes both CTAs land per stage
     static constexpr int STAGING_OFFSET = STAGES * STAGE_BYTES;   // 4 warps x 2 x (32 rows x 64 B)
-    static constexpr int STAGING_BYTES = 4 * 2 * 2048;
+    static constexpr int STAGING_BYTES = EPI_WARPS * 2 * 2048;
     static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
     static constexpr int VEC_BYTES = 2 * 3 * BN * 4;              // [acc parity][bias|wscale|gate][BN]
     static constexpr int BAR_OFFSET = VEC_OFFSET + VEC_BYTES;
@@ -86,7 +88,7 @@ struct PairLayout {
 };
 
 template <int KIND, int BN, int STAGES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     dmpq_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
@@ -120,7 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);
-            mbar_init(bar_tempty + 8 * a, 8);  // 4 epilogue warps x 2 CTAs
+            mbar_init(bar_tempty + 8 * a, 2 * EPI_WARPS);  // every epilogue warp of both CTAs
         }
         fence_barrier_init();
     }
@@ -224,7 +226,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         // output element and is the critical path for short-K layers, so
         // the math is packed fp32x2 (FFMA2/FMUL2/FADD2) and per-column vectors come from smem
         // as 128-bit broadcast loads.
-        const int q = warp & 3;
+        const int q = warp & 3;                 // TMEM lane quarter this warp may access
+        const int ew = warp - 4;                 // epilogue warp index
+        const int chalf = ew >> 2;               // column phase: chunks chalf, chalf + CSTEP, ...
+        constexpr int CSTEP = EPI_WARPS / 4;
         const int etid = threadIdx.x - 128;
         int local = 0;
         uint32_t chunk_ctr = 0;
@@ -232,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if constexpr (FP4) gg = __fmul_rn(*p.g_a, *p.g_w);
         else if constexpr (!I8) gg = 1.0f;   // BF16: y = fma(acc, 1, bias) = fl(acc + bias)
         const f2 gg2 = f2make(gg, gg);
-        const uint32_t staging = sbase + L::STAGING_OFFSET + q * 4096;
+        const uint32_t staging = sbase + L::STAGING_OFFSET + ew * 4096;
         const uint32_t vec_s = sbase + L::VEC_OFFSET;
         const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0;
         const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
@@ -244,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const int n0 = nt * BN;
             // per-column epilogue vectors of this tile -> smem (double-buffered by tile parity)
             const uint32_t vb = vec_s + acc * 3 * BN * 4;
-            for (int i = etid; i < BN; i += 128) {
+            for (int i = etid; i < BN; i += 32 * EPI_WARPS) {
                 const int col = n0 + i;
                 const bool ok = col < p.n;
                 const float bv = (ok && has_bias) ? p.bias[col] : -0.0f;   // fma(x, s, -0) == fl(x * s) exactly
@@ -254,7 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + (BN + i) * 4), "f"(wv) : "memory");
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + (2 * BN + i) * 4), "f"(gv) : "memory");
             }
-            named_bar_sync(1, 128);
+            named_bar_sync(1, 32 * EPI_WARPS);
             const int rowbase = mt * 256 + (int)rank * BM + q * 32;
             const int row = rowbase + lane;
             const bool row_ok = row < p.m;
@@ -264,12 +269,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
             tc_fence_after();
             const int n_here = min(BN, p.n - n0);
-            for (int c = 0; c < BN / 32; ++c) {
-                if (c * 32 >= n_here) break;
+            const int nch_here = (n_here + 31) >> 5;
+            const int my_last = nch_here > chalf ? chalf + ((nch_here - 1 - chalf) / CSTEP) * CSTEP : -1;
+            if (my_last < 0) {   // no chunk for this warp in a narrow tile: release TMEM right away
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
+            }
+            for (int c = chalf; c < nch_here; c += CSTEP) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
-                if (c * 32 + 32 >= n_here) {
+                if (c == my_last) {   // this warp's last TMEM read of the accumulator
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
@@ -299,15 +310,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                         y[2 * v4 + 1] = fma2(mul2(a1, sa2), f2make(w2, w3), bb1);
                     }
                 }
-                if (has_gelu) {
+                if (has_gelu) {   // GELU-tanh glue (R13), packed: 0.5x(1 + tanh(k0 (x + k1 x^3)))
+                    const f2 k1 = f2make(0.044715f, 0.044715f), k0 = f2make(0.7978845608028654f, 0.7978845608028654f);
+                    const f2 hf = f2make(0.5f, 0.5f);
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        float lo = f2lo(y[j]), hi = f2hi(y[j]);
-                        lo = __fmul_rn(__fmul_rn(0.5f, lo), __fadd_rn(1.0f, tanh_approx(__fmul_rn(0.7978845608028654f,
-                                       __fadd_rn(lo, __fmul_rn(0.044715f, __fmul_rn(__fmul_rn(lo, lo), lo)))))));
-                        hi = __fmul_rn(__fmul_rn(0.5f, hi), __fadd_rn(1.0f, tanh_approx(__fmul_rn(0.7978845608028654f,
-                                       __fadd_rn(hi, __fmul_rn(0.044715f, __fmul_rn(__fmul_rn(hi, hi), hi)))))));
-                        y[j] = f2make(lo, hi);
+                        const f2 x = y[j];
+                        const f2 x3 = mul2(mul2(x, x), x);
+                        const f2 u = mul2(k0, fma2(k1, x3, x));
+                        const f2 t = f2make(tanh_approx(f2lo(u)), tanh_approx(f2hi(u)));
+                        const f2 h = mul2(hf, x);
+                        y[j] = fma2(h, t, h);
                     }
                 }
                 if (has_res && row_ok) {
@@ -469,7 +482,7 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     const int tiles = p.num_m_tiles * p.num_n_tiles;
     int clusters = num_sms() / 2;
     if (clusters > tiles) clusters = tiles;
-    kern<<<2 * clusters, 256, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, p);
+    kern<<<2 * clusters, 128 + 32 * EPI_WARPS, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, p);
     return check_launch("dmpq_gemm");
 }
 
@@ -479,9 +492,9 @@ using namespace dmpq;
 
 extern "C" dmpq_status dmpq_prepare(void) {
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_prepare: needs an sm_100 device");
-    dmpq_status rc = set_pair_attrs<0, 256, 6>();
-    if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 6>();
-    if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
+    dmpq_status rc = set_pair_attrs<0, 256, 5>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5>();
     return rc;
 }
 
@@ -523,17 +536,17 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
-        return launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
+        return launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st);
     } else if (A->fmt == DMPQ_FMT_BF16) {
         DMPQ_REQUIRE(A->codes && W->bf16_w && aligned16(A->codes) && aligned16(W->bf16_w), DMPQ_EALIGN,
                      "dmpq_gemm: BF16 path needs A->codes (bf16 activation) and W->bf16_w");
         p.kbytes = 2 * k;
-        return launch_gemm_pair<2, 256, 6>(p, A->codes, W->bf16_w, st);
+        return launch_gemm_pair<2, 256, 5>(p, A->codes, W->bf16_w, st);
     } else {
         DMPQ_REQUIRE(A->codes && A->row_scale && W->i8_codes && W->i8_scale && aligned16(A->codes) && aligned16(W->i8_codes),
                      DMPQ_EALIGN, "dmpq_gemm: INT8 operand pointers");
         p.kbytes = k;
         p.a_scale = A->row_scale; p.w_scale = W->i8_scale;
-        return launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);
+        return launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st);
     }
 }
