@@ -21,6 +21,8 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tmap.cuh"
+#include "quant.cuh"
 #include "sm100.cuh"
 
 namespace dmpq {
@@ -78,13 +80,18 @@ struct PairLayout {
     static constexpr int SFB_BYTES = FP4 ? 2 * 4 * 512 : 0;       // 2 row-tiles of atoms (256 B rows)
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
     static constexpr int PAIR_TX = 2 * STAGE_BYTES;               // bytes both CTAs land per stage
-    static constexpr int STAGING_OFFSET = STAGES * STAGE_BYTES;   // 4 warps x 2 x (32 rows x 64 B)
-    static constexpr int STAGING_BYTES = EPI_WARPS * 2 * 2048;
-    static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
+    static constexpr int STAGING_OFFSET = STAGES * STAGE_BYTES;   // per epilogue warp: STAGING_BUFS x (32 rows x 64 B)
     static constexpr int VEC_BYTES = 2 * 3 * BN * 4;              // [acc parity][bias|wscale|gate][BN]
+    static constexpr int SMEM_LIMIT = 232448;                     // 227 KB opt-in per CTA
+    // double-buffered output staging when it fits next to the stage ring, else single-buffered
+    static constexpr int STAGING_BUFS =
+        (STAGING_OFFSET + EPI_WARPS * 2 * 2048 + VEC_BYTES + 256 + 1024 <= SMEM_LIMIT) ? 2 : 1;
+    static constexpr int STAGING_BYTES = EPI_WARPS * STAGING_BUFS * 2048;
+    static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
     static constexpr int BAR_OFFSET = VEC_OFFSET + VEC_BYTES;
     static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;
     static_assert(STAGE_BYTES % 1024 == 0, "stage buffers must stay 1024-B aligned");
+    static_assert(TOTAL <= SMEM_LIMIT, "shared memory budget");
 };
 
 template <int KIND, int BN, int STAGES>
@@ -237,7 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         if constexpr (FP4) gg = __fmul_rn(*p.g_a, *p.g_w);
         else if constexpr (!I8) gg = 1.0f;   // BF16: y = fma(acc, 1, bias) = fl(acc + bias)
         const f2 gg2 = f2make(gg, gg);
-        const uint32_t staging = sbase + L::STAGING_OFFSET + ew * 4096;
+        const uint32_t staging = sbase + L::STAGING_OFFSET + ew * (L::STAGING_BUFS * 2048);
         const uint32_t vec_s = sbase + L::VEC_OFFSET;
         const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0;
         const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
@@ -341,8 +348,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     }
                 }
                 if (p.Y) {
-                    const uint32_t buf = staging + (chunk_ctr & 1) * 2048;
-                    if (lane == 0) bulk_wait_read1();   // the store issued from this buffer 2 chunks ago has read it
+                    const uint32_t buf = staging + (L::STAGING_BUFS == 2 ? (chunk_ctr & 1) * 2048 : 0);
+                    if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
+                        if constexpr (L::STAGING_BUFS == 2) bulk_wait_read1();
+                        else bulk_wait_read0();
+                    }
                     __syncwarp();
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
@@ -388,22 +398,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
 
 // ------------------------------------------------------------------ host side
 
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    });
-    return fn;
-}
 
 // 2-D uint8 tensor map over a [rows x row_bytes] row-major matrix, box 128 B x box_rows, 128-B swizzle.
 static bool make_tmap(CUtensorMap* tm, const void* base, int rows, int row_bytes, int box_rows) {
-    auto enc = get_encode_fn();
+    auto enc = tmap_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
@@ -417,7 +415,7 @@ static bool make_tmap(CUtensorMap* tm, const void* base, int rows, int row_bytes
 
 // 3-D view of a swizzled scale buffer: [row_tiles][kc4 atoms][128 x u32 (512 B)], box {128, 4, box_tiles}.
 static bool make_tmap_sf(CUtensorMap* tm, const void* base, int row_tiles, int kc4, int box_tiles) {
-    auto enc = get_encode_fn();
+    auto enc = tmap_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[3] = {128, (cuuint64_t)kc4, (cuuint64_t)row_tiles};
     cuuint64_t strides[2] = {512, (cuuint64_t)kc4 * 512};
@@ -431,7 +429,7 @@ static bool make_tmap_sf(CUtensorMap* tm, const void* base, int row_tiles, int k
 
 // bf16 output [rows x cols] (row stride ld elements), box 32 x 32, 64-B swizzle (epilogue TMA store).
 static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, int ld) {
-    auto enc = get_encode_fn();
+    auto enc = tmap_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
@@ -490,11 +488,28 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
 
 using namespace dmpq;
 
+// Stage-ring depth of the GEMM (tuning knob, DMPQ_GEMM_STAGES = 5 | 6; default 5: the 6-stage ring only fits with single-buffered output staging, measured slower on the N = 12288 layer).
+static int gemm_stages() {
+    static int st = [] {
+        const char* e = std::getenv("DMPQ_GEMM_STAGES");
+        return (e && std::atoi(e) == 6) ? 6 : 5;
+    }();
+    return st;
+}
+
 extern "C" dmpq_status dmpq_prepare(void) {
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_prepare: needs an sm_100 device");
-    dmpq_status rc = set_pair_attrs<0, 256, 5>();
-    if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5>();
-    if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5>();
+    dmpq_status rc = DMPQ_OK;
+    if (gemm_stages() == 5) {
+        rc = set_pair_attrs<0, 256, 5>();
+        if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5>();
+        if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5>();
+    } else {
+        rc = set_pair_attrs<0, 256, 6>();
+        if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 6>();
+        if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
+    }
+    if (rc == DMPQ_OK) rc = prepare_quant_tma();
     return rc;
 }
 
@@ -536,17 +551,20 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
-        return launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st);
+        return gemm_stages() == 5 ? launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st)
+                                 : launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
     } else if (A->fmt == DMPQ_FMT_BF16) {
         DMPQ_REQUIRE(A->codes && W->bf16_w && aligned16(A->codes) && aligned16(W->bf16_w), DMPQ_EALIGN,
                      "dmpq_gemm: BF16 path needs A->codes (bf16 activation) and W->bf16_w");
         p.kbytes = 2 * k;
-        return launch_gemm_pair<2, 256, 5>(p, A->codes, W->bf16_w, st);
+        return gemm_stages() == 5 ? launch_gemm_pair<2, 256, 5>(p, A->codes, W->bf16_w, st)
+                                 : launch_gemm_pair<2, 256, 6>(p, A->codes, W->bf16_w, st);
     } else {
         DMPQ_REQUIRE(A->codes && A->row_scale && W->i8_codes && W->i8_scale && aligned16(A->codes) && aligned16(W->i8_codes),
                      DMPQ_EALIGN, "dmpq_gemm: INT8 operand pointers");
         p.kbytes = k;
         p.a_scale = A->row_scale; p.w_scale = W->i8_scale;
-        return launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st);
+        return gemm_stages() == 5 ? launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st)
+                                 : launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);
     }
 }

@@ -6,7 +6,9 @@
 #include <cstring>
 #include <mutex>
 
+
 #include "common.cuh"
+#include "tmap.cuh"
 
 namespace dmpq {
 
@@ -53,6 +55,19 @@ bool device_is_sm100() {
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return false; }
     query_device(dev);
     return dev >= 0 && dev < 64 && g_cc[dev] == 100;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
 }
 
 }  // namespace dmpq

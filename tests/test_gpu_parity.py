@@ -72,7 +72,8 @@ def test_quantize_adversarial_rows(D, orc, k):
     saturating blocks (g far below amax/1344) and the R4 reciprocal tie vector."""
     x = synth.adversarial_rows(k)
     m = x.shape[0]
-    for g_val in (1.0, orc.global_scale(orc.amax_bf16(_u16(x)), 1344.0), 1e-3):
+    # g = 1e-30 / 1e30 are outside the fast block-scale path's guard (IEEE fallback)
+    for g_val in (1.0, orc.global_scale(orc.amax_bf16(_u16(x)), 1344.0), 1e-3, 1e-30, 1e30):
         g = torch.tensor([g_val], dtype=torch.float32, device="cuda")
         a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
         a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
@@ -222,6 +223,41 @@ def test_quantize_hadamard_bit_exact(D, orc, m, k, ln):
     c8, s8 = orc.int8_quantize_f32(y)
     assert np.array_equal(a8.codes.cpu().numpy(), c8)
     assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+
+
+@pytest.mark.parametrize("k", [128, 1920])
+def test_quantize_hadamard_adversarial_rows(D, orc, k):
+    """The Hadamard quantizer on the adversarial rows (zero, tiny, huge, constant rows,
+    saturating and E4M3-subnormal blocks) with global scales inside and outside the fast
+    block-scale path's guard range."""
+    x = synth.adversarial_rows(k)
+    m = x.shape[0]
+    y = orc.fht128(orc.bf16_to_f32(synth.bits(x)).reshape(m, k))
+    for g_val in (1.0, 1e-3, float(np.abs(y).max()) / 1344.0, 1e-30, 1e30):
+        g = torch.tensor([g_val], dtype=torch.float32, device="cuda")
+        a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+        a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+        D.dmpq_quantize_act(x.cuda(), out_i8=a8, out_fp4=a4, hadamard=True)
+        torch.cuda.synchronize()
+        c4, s4 = orc.nvfp4_quantize_f32(y, float(g.item()))
+        assert np.array_equal(a4.codes.cpu().numpy(), c4)
+        assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s4)
+        c8, s8 = orc.int8_quantize_f32(y)
+        assert np.array_equal(a8.codes.cpu().numpy(), c8)
+        assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+
+
+def test_fastmath_exhaustive(tmp_path):
+    """The quantizers' guarded fast division / reciprocal (csrc/fastmath.cuh) equal
+    __fdiv_rn / __frcp_rn on every float of their guard ranges (scripts/fastmath_check.cu)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "fmc")
+    subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                           "--fmad=false", "-o", exe, os.path.join(root, "scripts", "fastmath_check.cu")])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("n,k", [(128, 128), (256, 1920)])
