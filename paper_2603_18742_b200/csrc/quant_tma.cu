@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
 
     if (tid == 0) {
         prefetch_tmap(&tmX);
-        for (int j = 0; j < nbuf; ++j) mbar_init(bar0 + 8 * j, 1);
+        for (int j = 0; j < nbuf; ++j) {
+            mbar_init(bar0 + 8 * j, 1);                                 // full: TMA bytes landed
+            mbar_init(bar0 + 8 * (nbuf + j), (blockDim.x + 31) >> 5);   // empty: every warp done with it
+        }
         fence_barrier_init();
     }
     __syncthreads();
@@ -163,6 +166,15 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
         const bool row_live = row < p.m;
         const bool live = row_live && cvalid;
         const int s0 = (it & 1) * 4;   // reduction slots of this iteration
+        // refill the buffer of the previous iteration once every warp has released it (only
+        // thread 0 waits; the other warps run ahead), keeping nbuf - 1 row sets in flight
+        if (tid == 0 && it >= 1 && it - 1 + nbuf < iters) {
+            const int pb = (it - 1) % nbuf;
+            mbar_wait(bar0 + 8 * (nbuf + pb), ((it - 1) / nbuf) & 1);
+            mbar_arrive_expect_tx(bar0 + 8 * pb, tx_bytes);
+            tma_load_3d(sbase + pb * set_stride, &tmX, 0, 0, (set - (int)gridDim.x + nbuf * (int)gridDim.x) * R,
+                        bar0 + 8 * pb);
+        }
         mbar_wait(bar0 + 8 * b, (it / nbuf) & 1);
         const uint32_t L = (uint32_t)(grp * nch + t);
         const uint32_t line = sbase + b * set_stride + L * 128, sw = L & 7;
@@ -231,28 +243,28 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
             fht_stages_1_32(Y);
             // h = 64: lower lane keeps a + b, upper lane gets a - b = fma(-1, b, a) (exact
             // product, one rounding), exchanged through the two threads' own smem lines in
-            // two 128-byte halves; then * fl32(1/sqrt(128)).
+            // four 64-byte quarters; then * fl32(1/sqrt(128)).
             const uint32_t pl = sbase + b * set_stride + (L ^ 1u) * 128, psw = (L ^ 1u) & 7;
             const f2 sg = (t & 1) ? f2make(-1.0f, -1.0f) : f2make(1.0f, 1.0f);
             const f2 sc = f2make(0.08838834764831845f, 0.08838834764831845f);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 4; ++h) {   // four 64-byte quarters (keeps the partner values to 16 registers)
                 if (cvalid) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) sts_f2x2(line + ((u ^ sw) << 4), Y[16 * h + 2 * u], Y[16 * h + 2 * u + 1]);
+                    for (int u = 0; u < 4; ++u) sts_f2x2(line + ((u ^ sw) << 4), Y[8 * h + 2 * u], Y[8 * h + 2 * u + 1]);
                 }
                 __syncwarp();
-                f2 O[16];
+                f2 O[8];
                 if (cvalid) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) lds_f2x2(pl + ((u ^ psw) << 4), O[2 * u], O[2 * u + 1]);
+                    for (int u = 0; u < 4; ++u) lds_f2x2(pl + ((u ^ psw) << 4), O[2 * u], O[2 * u + 1]);
                 } else {
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) O[u] = f2make(0.0f, 0.0f);
+                    for (int u = 0; u < 8; ++u) O[u] = f2make(0.0f, 0.0f);
                 }
                 __syncwarp();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) Y[16 * h + i] = mul2(fma2(sg, Y[16 * h + i], O[i]), sc);
+                for (int i = 0; i < 8; ++i) Y[8 * h + i] = mul2(fma2(sg, Y[8 * h + i], O[i]), sc);
             }
         }
 
@@ -313,13 +325,11 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
                                        int8x4(mul2(Y[8 * j + 6], r2), mul2(Y[8 * j + 7], r2)));
             }
         }
-        // buffer b is free once every thread is past its reads (and exchange writes): refill it
+        // release buffer b: this warp's reads and exchange writes are done (the generic-proxy
+        // writes are ordered before the TMA refill by the proxy fence + mbarrier release/acquire)
         fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0 && it + nbuf < iters) {
-            mbar_arrive_expect_tx(bar0 + 8 * b, tx_bytes);
-            tma_load_3d(sbase + b * set_stride, &tmX, 0, 0, (set + nbuf * (int)gridDim.x) * R, bar0 + 8 * b);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
     }
     // zero the scale rows that pad m up to a multiple of 128 (read by the GEMM's M tail)
     if (want_fp4) {
@@ -400,7 +410,7 @@ dmpq_status launch_quant_tma(const QuantParams& p, bool hadamard, cudaStream_t s
     // ring depth: enough row sets in flight to cover HBM latency (about 48 KB or more per CTA)
     int nbuf = 2;
     while (nbuf < 4 && (nbuf + 1) * set_stride <= 96 * 1024 && nbuf * set_stride < 72 * 1024) ++nbuf;
-    const int smem = nbuf * set_stride + 8 * MAX_SEG * 4 + 8 * nbuf + 1024;
+    const int smem = nbuf * set_stride + 8 * MAX_SEG * 4 + 16 * nbuf + 1024;
     if (threads > MAX_THREADS || smem > MAX_SMEM)
         return set_error(DMPQ_ESHAPE, "dmpq_quantize_act: k=%d exceeds the chunk quantizer's limits", p.k);
     CUtensorMap tm;
