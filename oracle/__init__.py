@@ -83,6 +83,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_outlier_ratio.argtypes, L.oracle_outlier_ratio.restype = [P, LL, LL], ctypes.c_double
         L.oracle_tdc_skip.argtypes = [P, P, LL, P]
         L.oracle_amax_bf16.argtypes, L.oracle_amax_bf16.restype = [P, LL], F
+        L.oracle_cache_dequant.argtypes = [P, P, F, LL, P]
+        L.oracle_tdc_skip_nvfp4.argtypes = [P, P, P, F, LL, P]
+        L.oracle_block_stats_nvfp4.argtypes = [P, P, P, P, F, I, I, F, P, P, P, P]
         _lib = L
     return _lib
 
@@ -334,3 +337,40 @@ def tdc_skip(x_in, delta):
 def amax_bf16(x) -> float:
     xi = _u16(x).reshape(-1)
     return float(lib().oracle_amax_bf16(_p(xi), xi.size))
+
+
+# ----------------------------------------------------------------------------- compressed delta cache (R16)
+
+def cache_dequant(codes, sf, g: float) -> np.ndarray:
+    """dq = fl32(dec(code) * fl32(dec(s_b) * g)) of an NVFP4-compressed delta cache (R16)."""
+    c = np.ascontiguousarray(codes, dtype=np.uint8)
+    f = np.ascontiguousarray(sf, dtype=np.uint8)
+    n = c.size * 2
+    out = np.zeros(n, dtype=np.float32)
+    lib().oracle_cache_dequant(_p(c), _p(f), float(g), n, _p(out))
+    return out.reshape(c.shape[0], -1) if c.ndim == 2 else out
+
+
+def tdc_skip_nvfp4(x_in, codes, sf, g: float):
+    """TDC skip with the compressed cache (R16): X_out = bf16(X_in + dq)."""
+    xi = _u16(x_in).reshape(-1)
+    out = np.zeros_like(xi)
+    lib().oracle_tdc_skip_nvfp4(_p(xi), _p(np.ascontiguousarray(codes, dtype=np.uint8)),
+                                _p(np.ascontiguousarray(sf, dtype=np.uint8)), float(g), xi.size, _p(out))
+    return out.reshape(np.shape(x_in))
+
+
+def block_stats_nvfp4(x_in, x_out, codes_prev, sf_prev, g_prev: float, g_new: float):
+    """Refresh with the compressed cache (Eqs. 3, 8, 9; R16). Returns
+    (codes_new [m, h/2], sf_new [m, h/16], st[7], amax |d|)."""
+    xi = _u16(x_in)
+    xo = _u16(x_out)
+    m, h = xi.shape
+    cn = np.zeros((m, h // 2), dtype=np.uint8)
+    sn = np.zeros((m, h // 16), dtype=np.uint8)
+    st = np.zeros(7, dtype=np.float64)
+    am = np.zeros(1, dtype=np.float32)
+    lib().oracle_block_stats_nvfp4(_p(xi), _p(xo), _p(np.ascontiguousarray(codes_prev, dtype=np.uint8)),
+                                   _p(np.ascontiguousarray(sf_prev, dtype=np.uint8)), float(g_prev), m, h, float(g_new),
+                                   _p(cn), _p(sn), _p(st), _p(am))
+    return cn, sn, st, float(am[0])

@@ -512,3 +512,84 @@ float oracle_amax_bf16(const uint16_t* x, long long count) {
     }
     return a;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NVFP4-compressed delta cache ("Caching these residual deltas        */
+/* introduces only a small memory overhead, as they can be quantized to ultra- */
+/* low precision formats such as NVFP4"; SPEC S:330 cache_compress = nvfp4,    */
+/* S:365).  Reading R16: the cache of a block holds NVFP4(d) of the     */
+/* FP32 delta d = fl(y - x) of its last compute, quantized exactly as the      */
+/* FP32-input activation quantizer (oracle_nvfp4_quantize_f32, Eq. 2 with the  */
+/* two-level scale) with the cache's global scale g; codes [m x h/2] (element  */
+/* 2i in the low nibble), E4M3 scales [m x h/16] plain row-major.  The cached   */
+/* value it stands for is dq = fl(dec(code) * eff), eff = fl(dec(s_b) * g).     */
+/* ------------------------------------------------------------------------ */
+
+/* dq of every element of a compressed cache (FP32, one rounding per element) */
+void oracle_cache_dequant(const uint8_t* codes, const uint8_t* sf, float g, long long count, float* out) {
+    for (long long i = 0; i < count; ++i) {
+        uint8_t byte = codes[i / 2];
+        uint8_t nib = (i & 1) ? (byte >> 4) : (byte & 15);
+        float eff = (float)oracle_e4m3_decode(sf[i / 16]) * g;
+        out[i] = (float)oracle_e2m1_decode(nib) * eff;
+    }
+}
+
+/* TDC skip with the compressed cache ("X_out = X_in + Delta_tp"):
+ * x_out = bf16(fl(x + dq)). */
+void oracle_tdc_skip_nvfp4(const uint16_t* x_in, const uint8_t* codes, const uint8_t* sf, float g,
+                           long long count, uint16_t* x_out) {
+    for (long long i = 0; i < count; ++i) {
+        uint8_t byte = codes[i / 2];
+        uint8_t nib = (i & 1) ? (byte >> 4) : (byte & 15);
+        float eff = (float)oracle_e4m3_decode(sf[i / 16]) * g;
+        float dq = (float)oracle_e2m1_decode(nib) * eff;
+        x_out[i] = oracle_f32_to_bf16(oracle_bf16_to_f32(x_in[i]) + dq);
+    }
+}
+
+/* Refresh with the compressed cache: the statistics of oracle_block_stats with the
+ * previous delta Dp = dq of the cache as it stands (g_prev), then the cache is
+ * rewritten with NVFP4(d; g_new) (h % 16 == 0 elements per row) and amax = max |d|. */
+void oracle_block_stats_nvfp4(const uint16_t* x_in, const uint16_t* x_out, const uint8_t* codes_prev,
+                              const uint8_t* sf_prev, float g_prev, int m, int h, float g_new,
+                              uint8_t* codes_new, uint8_t* sf_new, double* st, float* amax) {
+    long long count = (long long)m * h;
+    long double s[7] = {0, 0, 0, 0, 0, 0, 0};
+    float a = 0.0f;
+    float d[16];
+    for (long long r = 0; r < m; ++r) {
+        for (int b = 0; b < h / 16; ++b) {
+            long long i0 = r * h + (long long)b * 16;
+            for (int i = 0; i < 16; ++i) {
+                long long e = i0 + i;
+                float x = oracle_bf16_to_f32(x_in[e]);
+                float y = oracle_bf16_to_f32(x_out[e]);
+                d[i] = y - x;
+                uint8_t byte = codes_prev[e / 2];
+                uint8_t nib = (e & 1) ? (byte >> 4) : (byte & 15);
+                float eff = (float)oracle_e4m3_decode(sf_prev[e / 16]) * g_prev;
+                long double dpv = (float)oracle_e2m1_decode(nib) * eff;
+                long double dnv = oracle_bf16_to_f32(oracle_f32_to_bf16(d[i]));
+                s[0] += fabsl((long double)d[i]);
+                s[1] += fabsl((long double)x);
+                s[2] += (long double)d[i] * (long double)d[i];
+                s[3] += (long double)x * (long double)x;
+                s[4] += dnv * dpv;
+                s[5] += dnv * dnv;
+                s[6] += dpv * dpv;
+                if (fabsf(d[i]) > a) a = fabsf(d[i]);
+            }
+        }
+    }
+    /* the previous cache is fully read above before it is overwritten */
+    for (long long r = 0; r < m; ++r) {
+        float row[h];
+        for (int j = 0; j < h; ++j)
+            row[j] = oracle_bf16_to_f32(x_out[r * h + j]) - oracle_bf16_to_f32(x_in[r * h + j]);
+        oracle_nvfp4_quantize_f32(row, 1, h, g_new, codes_new + r * (h / 2), sf_new + r * (h / 16));
+    }
+    (void)count;
+    for (int j = 0; j < 7; ++j) st[j] = (double)s[j];
+    *amax = a;
+}

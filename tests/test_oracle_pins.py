@@ -549,3 +549,76 @@ def test_gemm_bf16_exact_fractions(orc):
         for j in range(5):
             exact = sum(Fraction(float(xf[i, t])) * Fraction(float(wf[j, t])) for t in range(64)) + Fraction(float(b[j]))
             assert abs(Fraction(y[i, j]) - exact) <= abs(exact) * Fraction(1, 2 ** 50) + Fraction(1, 2 ** 80)
+
+
+# ----------------------------------------------------------------------------- compressed delta cache (R16)
+
+E2M1_GRID = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+
+
+def _exact_cache_case(m, h, seed):
+    """x_in on a 2^-4 grid in [-4, 4] and a delta on the E2M1 grid x 2^-3 with +-0.75
+    (= 6 x 2^-3) in every 16-block: y = x + delta is exactly bf16, d = delta exactly,
+    and NVFP4(d; g = 1) is lossless (block scale 2^-3 is an exact E4M3 value)."""
+    rng = np.random.default_rng(seed)
+    x = rng.integers(-64, 65, size=(m, h)) / 16.0
+    mag = E2M1_GRID[rng.integers(0, 8, size=(m, h))] * 0.125
+    d = mag * rng.choice([-1.0, 1.0], size=(m, h))
+    d.reshape(m, h // 16, 16)[:, :, 0] = 0.75 * rng.choice([-1.0, 1.0], size=(m, h // 16))
+    xt = torch.tensor(x, dtype=torch.float32).to(torch.bfloat16)
+    yt = torch.tensor(x + d, dtype=torch.float32).to(torch.bfloat16)
+    assert torch.equal(yt.float() - xt.float(), torch.tensor(d, dtype=torch.float32))
+    return xt, yt, d
+
+
+def test_cache_lossless_deltas_reduce_to_the_uncompressed_cache(orc):
+    """R16 pinned against the uncompressed TDC functions: with NVFP4-representable deltas
+    the compressed cache stores them exactly, so skip output and refresh statistics equal
+    oracle_tdc_skip / oracle_block_stats with a bf16 cache (independent code paths)."""
+    from paper_2603_18742_b200 import synth
+    m, h = 6, 64
+    xi, xo, d = _exact_cache_case(m, h, 1)
+    _, xp, dp = _exact_cache_case(m, h, 2)      # an earlier delta, also exactly representable
+    cp, sp = orc.nvfp4_quantize_f32(dp.astype(np.float32), 1.0)
+    assert np.array_equal(orc.cache_dequant(cp, sp, 1.0), dp.astype(np.float32))
+    cn, sn, st, am = orc.block_stats_nvfp4(synth.bits(xi), synth.bits(xo), cp, sp, 1.0, 1.0)
+    dp_bf16 = synth.bits(torch.tensor(dp, dtype=torch.float32).to(torch.bfloat16))
+    _, st_ref = orc.block_stats(synth.bits(xi), synth.bits(xo), dp_bf16)
+    np.testing.assert_array_equal(st, st_ref)
+    assert am == float(np.abs(d).max())
+    assert np.array_equal(orc.cache_dequant(cn, sn, 1.0), d.astype(np.float32))
+    d_bf16 = synth.bits(torch.tensor(d, dtype=torch.float32).to(torch.bfloat16))
+    assert np.array_equal(orc.tdc_skip_nvfp4(synth.bits(xi), cn, sn, 1.0), orc.tdc_skip(synth.bits(xi), d_bf16))
+
+
+def _dequant_numpy(codes, sf, g):
+    """dec(code) * fl32(dec(s) * g) written out with numpy float32 (SPEC S:370's
+    codec-composition oracle): nibble -> sign x E2M1 grid, E4M3 via torch."""
+    m = codes.shape[0]
+    nib = np.stack([codes & 15, codes >> 4], axis=-1).reshape(m, -1)
+    val = E2M1_GRID[nib & 7] * np.where(nib & 8, -1.0, 1.0)
+    s = torch.tensor(sf.reshape(-1)).view(torch.float8_e4m3fn).float().numpy().reshape(m, -1)
+    eff = (s.astype(np.float32) * np.float32(g)).astype(np.float32)
+    return (val.astype(np.float32) * np.repeat(eff, 16, axis=1)).astype(np.float32)
+
+
+def test_cache_skip_is_codec_composition(orc):
+    """Skip output equals x_in + dequant(quant_nvfp4(Delta)), composed by hand
+    (numpy float32 add, torch RNE to bf16); refresh amax and dequant error bound."""
+    from paper_2603_18742_b200 import synth
+    m, h = 5, 128
+    xi = synth.dit_activation(m, h, seed=11)
+    xo = (xi.float() + 0.05 * synth.dit_activation(m, h, seed=12).float()).to(torch.bfloat16)
+    d = (xo.float() - xi.float()).numpy()
+    g = orc.global_scale(float(np.abs(d).max()), 1344.0)
+    zc, zs = np.zeros((m, h // 2), np.uint8), np.zeros((m, h // 16), np.uint8)
+    cn, sn, st, am = orc.block_stats_nvfp4(synth.bits(xi), synth.bits(xo), zc, zs, 0.0, g)
+    assert am == float(np.abs(d).max())
+    assert st[4] == 0.0 and st[6] == 0.0           # an empty (zero) cache contributes nothing
+    dq = _dequant_numpy(cn, sn, g)
+    np.testing.assert_array_equal(orc.cache_dequant(cn, sn, g), dq)
+    eff = np.repeat((torch.tensor(sn.reshape(-1)).view(torch.float8_e4m3fn).float().numpy() * np.float32(g))
+                    .astype(np.float32).reshape(m, -1), 16, axis=1)
+    assert np.all(np.abs(dq.astype(np.float64) - d) <= eff)      # one E2M1 step at most
+    ref = (xi.float() + torch.tensor(dq)).to(torch.bfloat16)
+    assert np.array_equal(orc.tdc_skip_nvfp4(synth.bits(xi), cn, sn, g), synth.bits(ref))
