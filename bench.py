@@ -188,7 +188,7 @@ def run_ours(args):
     peaks, peak_kind = load_peaks()
 
     model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
-                     pdr=args.pdr, m_total=M)
+                     pdr=args.pdr, m_total=M, cache_nvfp4=args.cache_nvfp4)
     # block-0 input trajectory basis (this rank's rows)
     A, B = synth.trajectory_basis(m, H, seed=1000 + rank, device=dev)
 
@@ -358,6 +358,9 @@ def run_ours(args):
                    "parallelism": f"token-shard x{world}", "l2": "inputs larger than L2 (multi-GB working set per step)",
                    "cuda_graphs": not args.no_graphs,
                    "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr,
+                   "delta_cache": {"format": "nvfp4" if args.cache_nvfp4 else "bf16",
+                                   "bytes_per_rank": sum(d.nbytes() if args.cache_nvfp4 else d.numel() * 2
+                                                         for d in model.delta)},
                    "mix": mix},
         "block_step_ms": elapsed / args.steps / nb * 1e3,
         "breakdown_ms_per_step": breakdown,
@@ -390,6 +393,7 @@ def main():
     ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
     ap.add_argument("--pdr", action="store_true", help="enable the Purified Cache Refresh outlier gate (P:241, "
                     "NEXT-3; off by default: the north_star path is DMPQ + TDC)")
+    ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs --warmup >= 3", file=sys.stderr)

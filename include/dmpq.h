@@ -268,6 +268,38 @@ typedef enum { TDC_COMPUTE = 0, TDC_DECIDE_SKIP = 1 } tdc_decision;
 dmpq_status tdc_step(tdc_mode mode, const uint16_t* X_in, uint16_t* X_out, uint16_t* delta_cache, int m, int h,
                      double* stats_out, void* workspace, dmpq_stream_t s);
 
+/* NVFP4-compressed delta cache of one block ("they can be quantized to ultra-low
+ * precision formats such as NVFP4"; SPEC S:330 cache_compress = nvfp4; R16).
+ * Caller-owned device buffers; zero-initialise all three before the first refresh. */
+typedef struct {
+    uint8_t* codes;   /* [m x h/2]  E2M1 codes of the cached delta, element 2i in the low nibble */
+    uint8_t* sf;      /* [m x h/16] E4M3 block scales, plain row-major (not the MMA atom layout) */
+    float* g;         /* device scalar: the FP32 global scale the cache was written with */
+} tdc_nvfp4_cache;
+
+/* tdc_step with the compressed cache (R16). dq = fl(dec(code) * fl(dec(s_b) * g)).
+ *  SKIP:    X_out = bf16(fl(X_in + dq))  (X_out may alias X_in; g_new, amax_out,
+ *           stats_out and workspace unused, may be NULL).
+ *  REFRESH: d = fl(X_out - X_in); statistics as tdc_step(REFRESH) with Delta_new =
+ *           bf16(d) and Delta_prev = dq of the cache as it stands on entry; then the
+ *           cache is overwritten with NVFP4(d) under the global scale *g_new (the
+ *           FP32-input activation quantizer of Eq. 2: a_b, raw = fl(fl(a_b/6)/g),
+ *           E4M3, r = fl(1/eff), E2M1(d * r)), *cache->g = *g_new once every CTA has
+ *           read the old value, and max|d| is max-reduced into *amax_out (device,
+ *           non-negative floats; caller zeroes it). g_new: device scalar, normally the
+ *           delayed policy of R3 on the previous refresh's amax (dmpq_global_scale,
+ *           div 1344); tdc_delta_amax bootstraps the first refresh.
+ *  bf16 tensors [m x h], dense; h % 64 == 0. Memory: 0.5625 B per cached element
+ *  instead of 2 (bf16). */
+dmpq_status tdc_step_nvfp4(tdc_mode mode, const uint16_t* X_in, uint16_t* X_out, const tdc_nvfp4_cache* cache,
+                           const float* g_new, float* amax_out, int m, int h, double* stats_out, void* workspace,
+                           dmpq_stream_t s);
+
+/* max |fl(X_out - X_in)| over [m x h] max-reduced into *amax_out (device; caller zeroes
+ * it): the current amax that bootstraps a compressed cache's first global scale. */
+dmpq_status tdc_delta_amax(const uint16_t* X_in, const uint16_t* X_out, int m, int h, float* amax_out,
+                           dmpq_stream_t s);
+
 /* Host-side per-block TDC state. */
 typedef struct {
     int t_p;          /* last fully computed step (-1: none)           */

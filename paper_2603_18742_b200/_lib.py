@@ -59,6 +59,10 @@ class BlockStats(ctypes.Structure):
         return [self.sum_abs_d, self.sum_abs_x, self.sum_d2, self.sum_x2, self.dot_dd, self.sum_dn2, self.sum_dp2]
 
 
+class TdcNvfp4Cache(ctypes.Structure):
+    _fields_ = [("codes", c_void_p), ("sf", c_void_p), ("g", c_void_p)]
+
+
 class TdcState(ctypes.Structure):
     _fields_ = [("t_p", c_int), ("e_tp", c_double), ("e_acc", c_double), ("last", c_int), ("n_computed", c_int)]
 
@@ -87,6 +91,9 @@ _SIGNATURES = {
     "dmpq_gemm": ([ctypes.POINTER(Act), ctypes.POINTER(Weights), ctypes.POINTER(Epilogue), c_void_p, c_int, c_void_p,
                    c_void_p, c_void_p], c_int),
     "tdc_step": ([c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p], c_int),
+    "tdc_step_nvfp4": ([c_int, c_void_p, c_void_p, ctypes.POINTER(TdcNvfp4Cache), c_void_p, c_void_p, c_int, c_int,
+                        c_void_p, c_void_p, c_void_p], c_int),
+    "tdc_delta_amax": ([c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p], c_int),
     "tdc_init": ([ctypes.POINTER(TdcState)], None),
     "tdc_decide": ([ctypes.POINTER(TdcState), ctypes.POINTER(TdcConfig), c_int], c_int),
     "tdc_update": ([ctypes.POINTER(TdcState), ctypes.POINTER(TdcConfig), c_int, c_int, ctypes.POINTER(BlockStats)], None),

@@ -119,7 +119,7 @@ class DiTStack:
     def __init__(self, n_blocks: int, H: int, F: int, m_local: int, device, seed: int = 0,
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
-                 tau_outlier: float = 25.0, m_total: int | None = None):
+                 tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -130,17 +130,26 @@ class DiTStack:
         self.hadamard = hadamard      # online block-Hadamard smoothing (R14)
         self.pdr = pdr                # Purified Cache Refresh outlier gate (R15)
         self.tau_outlier = tau_outlier
+        self.cache_nvfp4 = cache_nvfp4  # NVFP4-compressed delta cache (R16)
         self.m_total = m_total if m_total is not None else m_local
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
         self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr)
                        for b in range(n_blocks)]
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
-        # [0] amax of the quantised values (NVFP4 global scales, R3); [1] max|x| of the layer inputs (PDR, R15)
-        self.amax = torch.zeros(2, n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
+        # one buffer for the per-step MAX all-reduce: [0] amax of the quantised values (NVFP4 global
+        # scales, R3); [1] max|x| of the layer inputs (PDR, R15); then max|d| of each block's last
+        # refresh (compressed delta cache, R16; kept across steps: skipped blocks do not refresh)
+        self.amax_all = torch.zeros(2 * n_blocks * N_SLOTS + n_blocks, dtype=torch.float32, device=self.device)
+        self.amax = self.amax_all[:2 * n_blocks * N_SLOTS].view(2, n_blocks, N_SLOTS)
+        self.delta_amax = self.amax_all[2 * n_blocks * N_SLOTS:]
+        self.g_delta = torch.zeros(n_blocks, dtype=torch.float32, device=self.device)
         self.row_abs = torch.zeros(n_blocks * N_SLOTS, m_local, dtype=torch.float32, device=self.device)
         self.ws = Workspace(m_local, H, F, self.device, self.g_table)
-        self.delta = [torch.zeros(m_local, H, dtype=torch.bfloat16, device=self.device) for _ in range(n_blocks)]
+        if cache_nvfp4:
+            self.delta = [D.DeltaCacheNvfp4(m_local, H, self.device) for _ in range(n_blocks)]
+        else:
+            self.delta = [torch.zeros(m_local, H, dtype=torch.bfloat16, device=self.device) for _ in range(n_blocks)]
         world = 1 if group is None else torch.distributed.get_world_size(group)
         self.world = world
         self.rank = 0 if group is None else torch.distributed.get_rank(group)
@@ -282,20 +291,38 @@ class DiTStack:
             self.prev_stats[bi] = None
             self.prev_skipped[bi] = False
             self.ratio[bi] = None
-            self.delta[bi].zero_()
+            if self.cache_nvfp4:
+                for t_ in (self.delta[bi].codes, self.delta[bi].sf, self.delta[bi].g):
+                    t_.zero_()
+            else:
+                self.delta[bi].zero_()
         self.g_table.fill_(1.0)
+        self.amax_all.zero_()
+        self.g_delta.zero_()
         self.records = []
 
-    def _block_work(self, b, x_in, x_out, d, fmts):
+    def _block_work(self, b, x_in, x_out, d, fmts, first=False):
         """Enqueue one block's kernels (capturable: no host sync, no allocation)."""
         if d == L.TDC_DECIDE_SKIP:
             with self._ev("tdc"):
-                D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
+                if self.cache_nvfp4:
+                    D.tdc_step_nvfp4(L.TDC_SKIP, x_in, x_out, self.delta[b])
+                else:
+                    D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
             return 0.0
         flops = self._compute_block(b, x_in, x_out, fmts)
         with self._ev("tdc"):
-            D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
-                       self.ws.tdc_ws)
+            st = self.stats_slots[self.rank, b, :L.STATS_LEN]
+            if self.cache_nvfp4:
+                am, g = self.delta_amax[b:b + 1], self.g_delta[b:b + 1]
+                am.zero_()
+                if first:   # no previous refresh: bootstrap the cache's global scale from the current amax
+                    D.tdc_delta_amax(x_in, x_out, am)
+                    D.dmpq_global_scale(am, 1344.0, g)
+                D.tdc_step_nvfp4(L.TDC_REFRESH, x_in, x_out, self.delta[b], g_new=g, amax_out=am, stats_out=st,
+                                 workspace=self.ws.tdc_ws)
+            else:
+                D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], st, self.ws.tdc_ws)
         return flops
 
     def step(self, x0: torch.Tensor, t: int) -> torch.Tensor:
@@ -321,8 +348,9 @@ class DiTStack:
                     if self.pdr and self.ratio[b] is not None:
                         fmts = D.dmpq_purify(fmts, [self.ratio[b][s] for s in SLOT_OF_LAYER], self.prev_skipped[b],
                                              self.tau_outlier)
+            first = self.cache_nvfp4 and d != L.TDC_DECIDE_SKIP and self.tdc[b].n_computed == 0
             if graphs:
-                key = (d, None if fmts is None else tuple(fmts))
+                key = (d, None if fmts is None else tuple(fmts), first)
                 g = self.graphs[b].get(key)
                 if g is None:
                     # capture on a side stream without a device-wide sync (torch.cuda.graph's
@@ -334,14 +362,14 @@ class DiTStack:
                     g = torch.cuda.CUDAGraph()
                     with torch.cuda.stream(self.capture_stream):
                         g.capture_begin(pool=self.graph_pool)
-                        self._block_work(b, x_in, x_out, d, fmts)
+                        self._block_work(b, x_in, x_out, d, fmts, first)
                         g.capture_end()
                     self.graphs[b][key] = g
                 g.replay()
                 flops = 0.0 if d == L.TDC_DECIDE_SKIP else 2.0 * self.m * (4 * self.H * self.H + 2 * self.H * self.F)
             else:
-                flops = self._block_work(b, x_in, x_out, d, fmts)
-            self.launches += 1 if d == L.TDC_DECIDE_SKIP else 11
+                flops = self._block_work(b, x_in, x_out, d, fmts, first)
+            self.launches += 1 if d == L.TDC_DECIDE_SKIP else (13 if first else 11)
             rec.linear_flops += flops
             rec.fmts.append(None if d == L.TDC_DECIDE_SKIP else fmts)
             rec.gammas.append(gamma)
@@ -361,10 +389,13 @@ class DiTStack:
                 self.launches += 1
             if self.group is not None and self.world > 1:
                 torch.distributed.all_reduce(self.stats_slots, op=torch.distributed.ReduceOp.SUM, group=self.group)
-                torch.distributed.all_reduce(self.amax, op=torch.distributed.ReduceOp.MAX, group=self.group)
+                torch.distributed.all_reduce(self.amax_all, op=torch.distributed.ReduceOp.MAX, group=self.group)
             # next step's NVFP4 global scales from the (all-rank) amax of this step (R3)
             D.dmpq_global_scale(self.amax[0].view(-1), 1344.0, self.g_table.view(-1))
             self.launches += 1
+            if self.cache_nvfp4:   # delta-cache scales for each block's next refresh (same delayed policy)
+                D.dmpq_global_scale(self.delta_amax, 1344.0, self.g_delta)
+                self.launches += 1
         # the D2H copy inside synchronises the stream (one exchange per step)
         stats = exchange(self.stats_slots, self.amax, None, 1)
         if self.pdr:

@@ -243,6 +243,42 @@ def tdc_step(mode: int, x_in: torch.Tensor, x_out: torch.Tensor, delta: torch.Te
                                          _ptr(workspace), _stream(x_in.device)))
 
 
+class DeltaCacheNvfp4:
+    """NVFP4-compressed delta cache of one block (R16): codes [m, h/2], row-major
+    E4M3 scales [m, h/16], and the device global scale it was written with. Zeroed."""
+
+    def __init__(self, m: int, h: int, device):
+        self.m, self.h = m, h
+        self.codes = torch.zeros(m, h // 2, dtype=torch.uint8, device=device)
+        self.sf = torch.zeros(m, h // 16, dtype=torch.uint8, device=device)
+        self.g = torch.zeros(1, dtype=torch.float32, device=device)
+
+    def c(self) -> L.TdcNvfp4Cache:
+        return L.TdcNvfp4Cache(_ptr(self.codes), _ptr(self.sf), _ptr(self.g))
+
+    def nbytes(self) -> int:
+        return self.codes.numel() + self.sf.numel() + 4
+
+
+def tdc_step_nvfp4(mode: int, x_in: torch.Tensor, x_out: torch.Tensor, cache: DeltaCacheNvfp4,
+                   g_new: torch.Tensor | None = None, amax_out: torch.Tensor | None = None,
+                   stats_out: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """tdc_step with the NVFP4-compressed cache (R16). SKIP: x_out = x_in + dq(cache).
+    REFRESH: stats vs dq(cache), cache <- NVFP4(x_out - x_in; g_new), amax |d| -> amax_out."""
+    m, h = x_in.shape
+    c = cache.c()
+    L.check("tdc_step_nvfp4", L.lib().tdc_step_nvfp4(mode, _ptr(x_in), _ptr(x_out), ctypes.byref(c), _ptr(g_new),
+                                                     _ptr(amax_out), m, h, _ptr(stats_out), _ptr(workspace),
+                                                     _stream(x_in.device)))
+
+
+def tdc_delta_amax(x_in: torch.Tensor, x_out: torch.Tensor, amax_out: torch.Tensor):
+    """max |x_out - x_in| max-reduced into amax_out (bootstraps a compressed cache's scale)."""
+    m, h = x_in.shape
+    L.check("tdc_delta_amax", L.lib().tdc_delta_amax(_ptr(x_in), _ptr(x_out), m, h, _ptr(amax_out),
+                                                     _stream(x_in.device)))
+
+
 def tdc_new_state() -> L.TdcState:
     st = L.TdcState()
     L.lib().tdc_init(ctypes.byref(st))

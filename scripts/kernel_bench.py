@@ -90,8 +90,18 @@ def bench_tdc(m, h):
     ws = torch.zeros(D.tdc_workspace_bytes(m, h), dtype=torch.uint8, device="cuda")
     t = timeit(lambda: D.tdc_step(1, xi, xo, dl, st, ws))
     t2 = timeit(lambda: D.tdc_step(0, xi, xo, dl))
+    cache = D.DeltaCacheNvfp4(m, h, "cuda")
+    g = torch.tensor([1e-3], device="cuda")
+    am = torch.zeros(1, device="cuda")
+    t3 = timeit(lambda: D.tdc_step_nvfp4(1, xi, xo, cache, g_new=g, amax_out=am, stats_out=st, workspace=ws))
+    t4 = timeit(lambda: D.tdc_step_nvfp4(0, xi, xo, cache))
+    b3, b4 = 4 + 2 * 0.5625, 4 + 0.5625     # bytes per element: x_in + x_out + cache read (+ write)
     return [dict(kernel="tdc_refresh", m=m, h=h, us=t * 1e6, gbs=m * h * 8 / t / 1e9, frac=m * h * 8 / t / 1e9 / PEAKS["hbm_gbs"]),
-            dict(kernel="tdc_skip", m=m, h=h, us=t2 * 1e6, gbs=m * h * 6 / t2 / 1e9, frac=m * h * 6 / t2 / 1e9 / PEAKS["hbm_gbs"])]
+            dict(kernel="tdc_skip", m=m, h=h, us=t2 * 1e6, gbs=m * h * 6 / t2 / 1e9, frac=m * h * 6 / t2 / 1e9 / PEAKS["hbm_gbs"]),
+            dict(kernel="tdc_refresh_nvfp4", m=m, h=h, us=t3 * 1e6, gbs=m * h * b3 / t3 / 1e9,
+                 frac=m * h * b3 / t3 / 1e9 / PEAKS["hbm_gbs"]),
+            dict(kernel="tdc_skip_nvfp4", m=m, h=h, us=t4 * 1e6, gbs=m * h * b4 / t4 / 1e9,
+                 frac=m * h * b4 / t4 / 1e9 / PEAKS["hbm_gbs"])]
 
 
 def main():

@@ -54,6 +54,15 @@ def test_validation_without_gpu(L):
     assert rc == L.DMPQ_ESHAPE and b"k % 64" in lib.dmpq_last_error()
     rc = lib.tdc_step(7, None, None, None, 1, 8, None, None, None)
     assert rc == L.DMPQ_EINVAL
+    cache = L.TdcNvfp4Cache(16, 16, 16)
+    rc = lib.tdc_step_nvfp4(L.TDC_SKIP, None, None, ctypes.byref(cache), None, None, 4, 96, None, None, None)
+    assert rc == L.DMPQ_ESHAPE and b"h % 64" in lib.dmpq_last_error()
+    rc = lib.tdc_step_nvfp4(L.TDC_SKIP, None, None, None, None, None, 4, 128, None, None, None)
+    assert rc == L.DMPQ_EINVAL
+    rc = lib.tdc_step_nvfp4(L.TDC_REFRESH, ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.byref(cache), None, None,
+                            4, 128, None, None, None)
+    assert rc == L.DMPQ_EINVAL   # X_out aliases X_in
+    assert lib.tdc_delta_amax(None, None, 4, 12, None, None) == L.DMPQ_ESHAPE
 
 
 def test_derive_tau_matches_oracle(L, orc):

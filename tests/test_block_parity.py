@@ -37,10 +37,20 @@ def close_bf16(gpu_bf16, ref64, rel=2.0 ** -7):
 
 
 MODES = {
-    # name: (hadamard, pdr, tau_outlier)
-    "dmpq_tdc": (False, False, 25.0),
-    "hadamard_pdr": (True, True, 9.0),   # tau_outlier between the O-input and FFN2-input ratios: mixed BF16
+    # name: (hadamard, pdr, tau_outlier, NVFP4-compressed delta cache, TDC tau)
+    "dmpq_tdc": (False, False, 25.0, False, 0.003),
+    "hadamard_pdr": (True, True, 9.0, False, 0.003),   # tau_outlier between the O-input and FFN2-input ratios: mixed BF16
+    # the compressed cache's quantization noise enters Eq. 9 (E >= ~eps^2/2 ~ 0.004 here, R16): a looser tau
+    # so that the trajectory still skips
+    "hadamard_cache_nvfp4": (True, False, 25.0, True, 0.02),
 }
+
+
+def _cache_state(stack):
+    d = stack.delta[0]
+    if stack.cache_nvfp4:
+        return (d.codes.clone().cpu().numpy(), d.sf.clone().cpu().numpy(), float(d.g.item()))
+    return d.clone().cpu()
 
 
 @pytest.fixture(scope="module", params=sorted(MODES))
@@ -52,22 +62,23 @@ def run(request):
     build.build()
     dev = torch.device("cuda")
     M, H, F, T = 256, 128, 512, 6
-    had, pdr, tau_o = MODES[request.param]
+    had, pdr, tau_o, c4, tau_c = MODES[request.param]
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
-    stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o)
+    stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o,
+                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2))
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):
         x = synth.trajectory_input(A, B, t, 50).to(dev)
         cap = {}
         stack.capture = cap
-        d0 = stack.delta[0].clone()
+        d0 = _cache_state(stack)
         g_before = stack.g_table.clone()
         ratio_before = None if stack.ratio[0] is None else list(stack.ratio[0])
         stack.step(x, t)
         stats = stack.end_step(t)
         rec = stack.records[-1]
-        steps.append(dict(t=t, cap=cap, x=x.cpu(), delta_prev=d0.cpu(), delta_new=stack.delta[0].clone().cpu(),
+        steps.append(dict(t=t, cap=cap, x=x.cpu(), delta_prev=d0, delta_new=_cache_state(stack),
                           stats=stats[0].copy(), fmts=rec.fmts[0], decision=rec.decisions[0],
                           g=g_before.cpu(), out=stack.x_buf[0].clone().cpu(), ratio=ratio_before,
                           amax_in=stack.amax[1, 0].cpu().numpy().copy()))
@@ -164,8 +175,16 @@ def test_stages_teacher_forced(run, orc):
         else:
             close_bf16(cap["x_out"], xmid + gate2[None, :] * y2)
         # TDC refresh on the GPU's X_in / X_out / previous delta
-        dn, sref = orc.block_stats(bits(cap["x_in"]), bits(cap["x_out"]), bits(st["delta_prev"]))
-        assert np.array_equal(bits(st["delta_new"]), dn)
+        if stack.cache_nvfp4:
+            (cp, sp, gp), (cn_, sn_, gn) = st["delta_prev"], st["delta_new"]
+            if gp == 0.0:   # first refresh: the scale was bootstrapped from this step's amax
+                d_ = f32(cap["x_out"]) - f32(cap["x_in"])
+                assert gn == orc.global_scale(float(np.abs(d_).max()), 1344.0)
+            cn, sn, sref, _ = orc.block_stats_nvfp4(bits(cap["x_in"]), bits(cap["x_out"]), cp, sp, gp, gn)
+            assert np.array_equal(cn_, cn) and np.array_equal(sn_, sn)
+        else:
+            dn, sref = orc.block_stats(bits(cap["x_in"]), bits(cap["x_out"]), bits(st["delta_prev"]))
+            assert np.array_equal(bits(st["delta_new"]), dn)
         np.testing.assert_allclose(st["stats"][:4], sref[:4], rtol=4.2e-7)
         np.testing.assert_allclose(st["stats"][4:7], sref[4:], rtol=1e-12, atol=1e-300)
     assert n_checked >= 3
@@ -246,7 +265,14 @@ def test_pdr_ratio_matches_oracle(run, orc):
 def test_skip_output_matches_oracle(run, orc):
     """A skipped step's output is X_in + Delta_tp exactly."""
     stack, steps = run
+    n = 0
     for i, st in enumerate(steps):
         if st["decision"] == 1:
-            ref = orc.tdc_skip(bits(st["x"]), bits(st["delta_prev"]))
+            if stack.cache_nvfp4:
+                cp, sp, gp = st["delta_prev"]
+                ref = orc.tdc_skip_nvfp4(bits(st["x"]), cp, sp, gp)
+            else:
+                ref = orc.tdc_skip(bits(st["x"]), bits(st["delta_prev"]))
             assert np.array_equal(bits(st["out"]), ref)
+            n += 1
+    assert n >= 1, "the trajectory should exercise at least one skip"

@@ -202,6 +202,52 @@ def test_tdc_refresh_and_skip(D, orc, m, h):
     assert np.array_equal(synth.bits(x.cpu()), orc.tdc_skip(_u16(xi), dn_ref))
 
 
+@pytest.mark.parametrize("m,h", [(1, 64), (256, 128), (1000, 1920), (777, 3072)])
+def test_tdc_nvfp4_cache(D, orc, m, h):
+    """NVFP4-compressed delta cache (R16): bootstrap amax, two refreshes (the second
+    against the first's compressed cache, delayed scale), skip (also in place): codes,
+    scales, amax, cache scale and outputs bit-exact; statistics as the bf16 cache path."""
+    act = lambda s_: synth.dit_activation(m, h, seed=s_, outlier_frac=0, tail_frac=0)
+    xi1 = act(m + 1)
+    xo1 = (xi1.float() + 0.05 * act(m + 2).float()).to(torch.bfloat16)
+    xi2 = act(m + 3)
+    xo2 = (xi2.float() + 0.04 * act(m + 4).float()).to(torch.bfloat16)
+    cache = D.DeltaCacheNvfp4(m, h, "cuda")
+    ws = torch.zeros(D.tdc_workspace_bytes(m, h), dtype=torch.uint8, device="cuda")
+    am0 = torch.zeros(1, device="cuda")
+    D.tdc_delta_amax(xi1.cuda(), xo1.cuda(), am0)
+    torch.cuda.synchronize()
+    d1 = xo1.float().numpy() - xi1.float().numpy()
+    assert am0.item() == float(np.abs(d1).max())
+    g1 = torch.tensor([orc.global_scale(am0.item(), 1344.0)], device="cuda")
+    zc, zs = np.zeros((m, h // 2), np.uint8), np.zeros((m, h // 16), np.uint8)
+    prev = (zc, zs, 0.0)
+    for (xi, xo, g) in ((xi1, xo1, g1), (xi2, xo2, None)):
+        if g is None:   # delayed policy: the previous refresh's amax
+            g = torch.tensor([orc.global_scale(am.item(), 1344.0)], device="cuda")
+        am = torch.zeros(1, device="cuda")
+        stats = torch.zeros(7, dtype=torch.float64, device="cuda")
+        D.tdc_step_nvfp4(1, xi.cuda(), xo.cuda(), cache, g_new=g, amax_out=am, stats_out=stats, workspace=ws)
+        torch.cuda.synchronize()
+        cn, sn, st_ref, am_ref = orc.block_stats_nvfp4(_u16(xi), _u16(xo), prev[0], prev[1], prev[2], g.item())
+        assert np.array_equal(cache.codes.cpu().numpy(), cn)
+        assert np.array_equal(cache.sf.cpu().numpy(), sn)
+        assert cache.g.item() == g.item() and am.item() == am_ref
+        st = stats.cpu().numpy()
+        np.testing.assert_allclose(st[:4], st_ref[:4], rtol=4.2e-7, atol=0)
+        np.testing.assert_allclose(st[4:], st_ref[4:], rtol=1e-12, atol=1e-300)
+        prev = (cn, sn, g.item())
+    xi3 = act(m + 5)
+    out = torch.empty_like(xi3).cuda()
+    D.tdc_step_nvfp4(0, xi3.cuda(), out, cache)
+    x = xi3.cuda().clone()
+    D.tdc_step_nvfp4(0, x, x, cache)
+    torch.cuda.synchronize()
+    ref = orc.tdc_skip_nvfp4(_u16(xi3), prev[0], prev[1], prev[2])
+    assert np.array_equal(synth.bits(out.cpu()), ref)
+    assert np.array_equal(synth.bits(x.cpu()), ref)
+
+
 @pytest.mark.parametrize("m,k,ln", [(5, 128, False), (130, 3072, True), (37, 1920, False), (33, 12288, False)])
 def test_quantize_hadamard_bit_exact(D, orc, m, k, ln):
     """Online block Hadamard fused into the quantizer (R14): codes and scales
