@@ -121,9 +121,9 @@ dmpq_status dmpq_pack_weights(const uint16_t* W, int n, int k, dmpq_weights* out
 
 #define DMPQ_PACK_HADAMARD 1u  /* rotate every row by the block FHT first (offline half of P:187's smoothing, R14) */
 
-/* dmpq_pack_weights with options: DMPQ_PACK_HADAMARD packs W~ = W . blockdiag(H_128)/sqrt(128)
- * (g_w from amax(W~)), so (H x) . W~^T = x . W^T for activations quantised with
- * DMPQ_QF_HADAMARD. k % 128 == 0 then. */
+/* dmpq_pack_weights with options: DMPQ_PACK_HADAMARD packs W~ = 2^-7 W . blockdiag(H_128)
+ * (Sylvester, entries +-1; g_w from amax(W~)), so (H x) . W~^T = x . W^T for activations
+ * quantised with DMPQ_QF_HADAMARD (R14). k % 128 == 0 then. */
 dmpq_status dmpq_pack_weights_ex(const uint16_t* W, int n, int k, uint32_t flags, dmpq_weights* out, dmpq_stream_t s);
 
 /* ========================================================================== */
@@ -173,8 +173,9 @@ void dmpq_purify(const double* ratio, int n_layers, int prev_skipped, double tau
 
 #define DMPQ_QF_LAYERNORM 1u  /* normalise each row first: h = (x - mean)/sqrt(var + eps), no affine (block glue) */
 #define DMPQ_QF_WRITE_H   2u  /* also store the bf16 values that were quantised into h_out (before any rotation) */
-#define DMPQ_QF_HADAMARD  4u  /* rotate every 128-element block by the normalized Sylvester FHT before quantising
-                                 (P:187 online block Hadamard, R14); pair with weights packed with DMPQ_PACK_HADAMARD */
+#define DMPQ_QF_HADAMARD  4u  /* rotate every 128-element block by the Sylvester FHT (entries +-1, FP32 butterflies)
+                                 before quantising (P:187 online block Hadamard, R14); pair with weights packed
+                                 with DMPQ_PACK_HADAMARD, which carry the 2^-7 normalization */
 
 typedef struct {
     uint32_t flags;

@@ -217,8 +217,9 @@ def pack_weights(w_bf16: np.ndarray):
 
 
 def fht128(x) -> np.ndarray:
-    """Normalized Sylvester block Hadamard over 128-element blocks of the last axis
-    (reading R14), fp32 butterflies in the fixed stage order."""
+    """Sylvester block Hadamard y = H_128 x over 128-element blocks of the last axis
+    (reading R14: entries +-1, the 1/128 normalization rides on the weights),
+    fp32 butterflies in the fixed stage order."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     assert x.shape[-1] % 128 == 0
     y = np.empty_like(x)

@@ -193,15 +193,15 @@ long long oracle_sf_offset(int r, int c, int k) {
 /* ------------------------------------------------------------------------ */
 /* Online block Hadamard smoothing ("we apply a Fast Hadamard Transform  */
 /* (FHT) over local activation blocks (B=128)").  Reading R14: the   */
-/* normalized Sylvester-ordered transform y = H_128 x / sqrt(128) per 128-block, */
-/* evaluated as the fast transform in FP32 exactly in this order: stages        */
-/* h = 1, 2, 4, ..., 64; within a stage every pair (i, i+h) with (i & h) == 0   */
-/* becomes (fl(a + b), fl(a - b)); then every element is multiplied by          */
-/* fl32(1/sqrt(128)).                                                            */
+/* Sylvester-ordered transform y = H_128 x per 128-block (entries +-1, no       */
+/* normalization on the activation side), evaluated as the fast transform in   */
+/* FP32 exactly in this order: stages h = 1, 2, 4, ..., 64; within a stage     */
+/* every pair (i, i+h) with (i & h) == 0 becomes (fl(a + b), fl(a - b)).  The   */
+/* normalization H^T H = 128 I is carried by the weights as the exact power of  */
+/* two 2^-7 (oracle_pack_weights_hadamard), so (H x) . (2^-7 H w) = x . w.     */
 /* ------------------------------------------------------------------------ */
 
 void oracle_fht128_f32(const float* x, float* y, long long n) {
-    const float s = (float)(1.0 / sqrt(128.0));
     for (long long b0 = 0; b0 < n; b0 += 128) {
         float v[128];
         for (int i = 0; i < 128; ++i) v[i] = x[b0 + i];
@@ -212,7 +212,7 @@ void oracle_fht128_f32(const float* x, float* y, long long n) {
                     v[i] = a + b;
                     v[i + h] = a - b;
                 }
-        for (int i = 0; i < 128; ++i) y[b0 + i] = v[i] * s;
+        for (int i = 0; i < 128; ++i) y[b0 + i] = v[i];
     }
 }
 
@@ -345,14 +345,15 @@ void oracle_pack_weights(const uint16_t* w, int n, int k,
 }
 
 /* Weight pack with the offline Hadamard rotation (reading R14): every row of W
- * (nn.Linear [n x k]) gets the same block FHT along k as the activations, so
- * (H x) . (H w) = x . w; then the two packed forms of oracle_pack_weights from the
- * rotated FP32 weights (g_w from their amax). */
+ * (nn.Linear [n x k]) gets the same block FHT along k as the activations, times the
+ * exact power of two 2^-7 = 1/128, so (H x) . (2^-7 H w) = x . w; then the two packed
+ * forms of oracle_pack_weights from the rotated FP32 weights (g_w from their amax). */
 void oracle_pack_weights_hadamard(const uint16_t* w, int n, int k,
                                   uint8_t* fp4_codes, uint8_t* fp4_sf, float* fp4_g,
                                   int8_t* i8_codes, float* i8_scale, float* w_rot /* [n x k] scratch/out */) {
     for (size_t i = 0; i < (size_t)n * k; ++i) w_rot[i] = oracle_bf16_to_f32(w[i]);
     oracle_fht128_f32(w_rot, w_rot, (long long)n * k);
+    for (size_t i = 0; i < (size_t)n * k; ++i) w_rot[i] = w_rot[i] * 0.0078125f;   /* 2^-7, exact */
     float amax = 0.0f;
     for (size_t i = 0; i < (size_t)n * k; ++i)
         if (fabsf(w_rot[i]) > amax) amax = fabsf(w_rot[i]);

@@ -440,9 +440,9 @@ def _sylvester(n):
 
 
 def test_fht_one_hot_is_a_hadamard_row(orc):
-    """Sylvester H[i][j] = (-1)^popcount(i & j); a one-hot block maps to +-1/sqrt(128)
+    """Sylvester H[i][j] = (-1)^popcount(i & j); a one-hot block maps to the +-1 row
     exactly (every butterfly adds a value to zero)."""
-    s = np.float32(1.0 / np.sqrt(128.0))
+    s = np.float32(1.0)
     for j in (0, 1, 5, 64, 127):
         x = np.zeros((1, 128), np.float32)
         x[0, j] = 1.0
@@ -456,14 +456,16 @@ def test_fht_matches_dense_transform_and_is_an_involution(orc):
     x = rng.standard_normal((6, 384)).astype(np.float32)
     x[:, 7] *= 80.0
     y = orc.fht128(x)
-    H = _sylvester(128) / np.sqrt(128.0)
+    H = _sylvester(128)
     dense = (x.astype(np.float64).reshape(6, 3, 128) @ H.T).reshape(6, 384)
     assert np.max(np.abs(y - dense)) <= 1e-5 * np.max(np.abs(dense))
-    np.testing.assert_allclose(np.linalg.norm(y, axis=1), np.linalg.norm(x.astype(np.float64), axis=1), rtol=1e-6)
-    assert np.max(np.abs(orc.fht128(y) - x)) <= 1e-5 * np.max(np.abs(x))          # S:209 involution
-    # linear-layer transparency: (Hx).(Hw) == x.w
+    # Parseval for the unnormalized transform: ||Hx||^2 = 128 ||x||^2
+    np.testing.assert_allclose(np.linalg.norm(y, axis=1), np.sqrt(128.0) * np.linalg.norm(x.astype(np.float64), axis=1),
+                               rtol=1e-6)
+    assert np.max(np.abs(orc.fht128(y) / 128.0 - x)) <= 1e-5 * np.max(np.abs(x))   # H H = 128 I (S:209 involution)
+    # linear-layer transparency: (Hx).(2^-7 Hw) == x.w
     w = rng.standard_normal((4, 384)).astype(np.float32)
-    np.testing.assert_allclose(orc.fht128(x).astype(np.float64) @ orc.fht128(w).T.astype(np.float64),
+    np.testing.assert_allclose(orc.fht128(x).astype(np.float64) @ (orc.fht128(w) / 128.0).T.astype(np.float64),
                                x.astype(np.float64) @ w.T.astype(np.float64), rtol=1e-5, atol=1e-4)
 
 
@@ -481,7 +483,7 @@ def test_fht_smooths_channel_outliers_for_int8(orc):
         e_plain.append(np.linalg.norm(c * s[:, None] - xb) / np.linalg.norm(xb))
         y = orc.fht128(xb)
         c2, s2 = orc.int8_quantize_f32(y)
-        back = orc.fht128((c2 * s2[:, None]).astype(np.float32))
+        back = orc.fht128((c2 * s2[:, None]).astype(np.float32)) / 128.0
         e_fht.append(np.linalg.norm(back - xb) / np.linalg.norm(xb))
     assert np.mean(e_fht) < 0.5 * np.mean(e_plain)
 
@@ -502,7 +504,7 @@ def test_pack_weights_hadamard(orc):
     rng = np.random.default_rng(24)
     w = bf16_bits((rng.standard_normal((32, 256)) / 16).astype(np.float32))
     pk = orc.pack_weights_hadamard(w)
-    wr = orc.fht128(bf16_vals(w))
+    wr = orc.fht128(bf16_vals(w)) * np.float32(2.0 ** -7)
     assert pk["fp4_g"] == orc.global_scale(float(np.abs(wr).max()), 2688.0)
     c, s = orc.nvfp4_quantize_f32(wr, pk["fp4_g"])
     assert np.array_equal(c, pk["fp4_codes"]) and np.array_equal(s, pk["fp4_sf"])
