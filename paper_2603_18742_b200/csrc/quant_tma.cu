@@ -11,7 +11,8 @@
 // registers or load instructions spent on prefetching; each thread then reads its own line
 // with conflict-free 16-byte loads (the swizzle spreads 8 consecutive lines over all banks).
 // Hadamard: FHT stages h = 1..32 run in registers on packed fp32 pairs; stage h = 64 pairs
-// chunk t with chunk t^1 (the neighbouring lane) through the two threads' own smem lines.
+// chunk t with chunk t^1 (the neighbouring lane) through the two threads' own smem lines;
+// no normalization (the packed weights carry the exact 2^-7, R14).
 // Row reductions (LN mean/var, INT8 row max, PDR sums) are fixed-order: 16-lane segment
 // shuffles, then the row's segments summed in order after one CTA barrier (deterministic).
 #include <algorithm>
@@ -243,10 +244,9 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
             fht_stages_1_32(Y);
             // h = 64: lower lane keeps a + b, upper lane gets a - b = fma(-1, b, a) (exact
             // product, one rounding), exchanged through the two threads' own smem lines in
-            // four 64-byte quarters; then * fl32(1/sqrt(128)).
+            // four 64-byte quarters. No normalization: the weights carry 2^-7 (R14).
             const uint32_t pl = sbase + b * set_stride + (L ^ 1u) * 128, psw = (L ^ 1u) & 7;
             const f2 sg = (t & 1) ? f2make(-1.0f, -1.0f) : f2make(1.0f, 1.0f);
-            const f2 sc = f2make(0.08838834764831845f, 0.08838834764831845f);
 #pragma unroll
             for (int h = 0; h < 4; ++h) {   // four 64-byte quarters (keeps the partner values to 16 registers)
                 if (cvalid) {
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
                 }
                 __syncwarp();
 #pragma unroll
-                for (int i = 0; i < 8; ++i) Y[8 * h + i] = mul2(fma2(sg, Y[8 * h + i], O[i]), sc);
+                for (int i = 0; i < 8; ++i) Y[8 * h + i] = fma2(sg, Y[8 * h + i], O[i]);
             }
         }
 
