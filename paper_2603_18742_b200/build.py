@@ -32,7 +32,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps.append(os.path.join(os.path.dirname(HERE), "include", "dmpq.h"))
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
-    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB, *srcs, "-lcuda" if False else "-ldl"]
+    extra = os.environ.get("DMPQ_NVCC_EXTRA", "").split()   # development experiments (e.g. -DQUANT_CH32_REGS=96)
+    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", LIB, *srcs, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
