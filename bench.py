@@ -370,6 +370,26 @@ def run_ours(args):
                     "by_format": by_fmt,
                     "timing": "CUDA events around every GEMM launch on its stream, eager replay of the timed steps"}
 
+    # ---- optional bounds: all-NVFP4 and all-INT8 steps without TDC skips
+    bounds = None
+    if args.bounds:
+        bounds = {}
+        for name, fmt in (("all_nvfp4_no_skip", D.FMT_NVFP4), ("all_int8_no_skip", D.FMT_INT8)):
+            model.force_fmt, model.tdc_enabled = fmt, False
+            warmup()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record()
+            fl0 = sum(r.linear_flops for r in model.records)
+            for i in range(args.steps):
+                t = args.warmup + i
+                model.step(steps_inputs[t], t)
+                model.end_step(t)
+            b1.record()
+            torch.cuda.synchronize()
+            bt, bfl = allmax_sum([b0.elapsed_time(b1) * 1e-3, sum(r.linear_flops for r in model.records) - fl0])
+            bounds[name] = {"ms_per_step": bt / args.steps * 1e3, "tflops": bfl / bt / 1e12}
+        model.force_fmt, model.tdc_enabled = None, True
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, secs, sample = cpu_oracle_sample(H, F, 4, mix["nvfp4_layer_frac"])
@@ -390,6 +410,7 @@ def run_ours(args):
                                                          for d in model.delta)},
                    "mix": mix},
         "block_step_ms": elapsed / args.steps / nb * 1e3,
+        "bounds": bounds,
         "breakdown_ms_per_step": breakdown,
         "effective_tflops_dense_equiv": dense_flops / elapsed / 1e12,
         "wall_s_timed": wall,
@@ -421,6 +442,8 @@ def main():
     ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
     ap.add_argument("--pdr", action="store_true", help="enable the Purified Cache Refresh outlier gate (P:241, "
                     "NEXT-3; off by default: the north_star path is DMPQ + TDC)")
+    ap.add_argument("--bounds", action="store_true", help="also time all-NVFP4 and all-INT8 steps without skips "
+                    "(SURVEY 8(d) bounds)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
     args = ap.parse_args()
     if args.warmup < 3:
