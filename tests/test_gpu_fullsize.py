@@ -86,3 +86,75 @@ def test_fullsize_tdc(D, orc):
     s = stats.cpu().numpy()
     np.testing.assert_allclose(s[:4], st[:4], rtol=4.2e-7)
     np.testing.assert_allclose(s[4:], st[4:], rtol=1e-12)
+
+
+@pytest.mark.parametrize("n,k,ln", [(3072, 3072, True), (3072, 12288, False)])
+def test_fullsize_hadamard_sampled(D, orc, n, k, ln):
+    """The bench's default path at full size: LN (attention / FFN1 inputs) + online block
+    Hadamard quantizer (both formats in one pass) against Hadamard-packed weights (R14)."""
+    x = synth.dit_activation(M, k, seed=k + 1) if k == 3072 else synth.ffn2_activation(M, k, seed=k + 1)
+    xd = x.cuda()
+    w, b = synth.linear_weight_device(n, k, seed=n + k + 1, device="cuda")
+    pw = D.dmpq_pack_weights(w, b, hadamard=True)
+    h = torch.empty(M, k, dtype=torch.bfloat16, device="cuda") if ln else None
+    g = torch.tensor([0.02], device="cuda")
+    amax = torch.zeros(1, device="cuda")
+    a8 = D.QuantAct.empty(D.FMT_INT8, M, k, "cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, M, k, "cuda", g=g)
+    D.dmpq_quantize_act(xd, out_i8=a8, out_fp4=a4, amax_out=amax, layernorm=ln, h_out=h, hadamard=True)
+    y8 = torch.empty(M, n, dtype=torch.bfloat16, device="cuda")
+    y4 = torch.empty(M, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a8, pw, Y=y8)
+    D.dmpq_gemm(a4, pw, Y=y4)
+    torch.cuda.synchronize()
+    pk = orc.pack_weights_hadamard(synth.bits(w.cpu()))
+    assert np.array_equal(pw.i8_codes.cpu().numpy(), pk["i8_codes"])
+    assert np.array_equal(pw.i8_scale.cpu().numpy(), pk["i8_scale"])
+    assert pw.fp4_g.item() == pk["fp4_g"]
+    src = synth.bits(h.cpu()) if ln else synth.bits(x)
+    bias = b.cpu().numpy()
+    c8_all, s8_all = a8.codes.cpu().numpy(), a8.row_scale.cpu().numpy()
+    c4_all, sf4 = a4.codes.cpu().numpy(), orc.sf_unswizzle(a4.sf.cpu().numpy(), M, k)
+    for r in sample_rows(M, seed=1):
+        y = orc.fht128(orc.bf16_to_f32(src[r:r + 1]).reshape(1, k))
+        c8, s8 = orc.int8_quantize_f32(y)
+        assert np.array_equal(c8_all[r:r + 1], c8) and s8_all[r] == s8[0], r
+        c4, s4 = orc.nvfp4_quantize_f32(y, 0.02)
+        assert np.array_equal(c4_all[r:r + 1], c4) and np.array_equal(sf4[r:r + 1], s4), r
+        _, yr8 = orc.gemm_int8(c8, s8, pk["i8_codes"], pk["i8_scale"], bias)
+        assert torch.equal(y8[r:r + 1].cpu(), torch.from_numpy(yr8).to(torch.bfloat16)), r
+        yr4 = orc.gemm_nvfp4(c4, s4, 0.02, pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"], bias)
+        got = y4[r].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got - yr4[0]) <= 4e-3 * np.linalg.norm(yr4[0]), r
+    # the tensor amax is a property of every row: check it over all rows of the sample
+    assert amax.item() >= float(np.abs(orc.fht128(orc.bf16_to_f32(src[:256]).reshape(256, k))).max())
+
+
+def test_fullsize_tdc_nvfp4_cache(D, orc):
+    """Compressed delta cache (R16) at full size: refresh against a compressed cache, skip."""
+    H = 3072
+    act = lambda s_: synth.dit_activation(M, H, seed=s_, outlier_frac=0, tail_frac=0)
+    xi, xo = act(11), None
+    xo = (xi.float() + 0.01 * act(12).float()).to(torch.bfloat16)
+    rng = np.random.default_rng(5)
+    cp = rng.integers(0, 256, size=(M, H // 2), dtype=np.uint8)
+    sp = rng.integers(0x20, 0x38, size=(M, H // 16), dtype=np.uint8)   # E4M3 0.0078 .. 1.0
+    cache = D.DeltaCacheNvfp4(M, H, "cuda")
+    cache.codes.copy_(torch.from_numpy(cp))
+    cache.sf.copy_(torch.from_numpy(sp))
+    cache.g.fill_(0.01)
+    g_new = torch.tensor([orc.global_scale(float((xo.float() - xi.float()).abs().max()), 1344.0)], device="cuda")
+    am = torch.zeros(1, device="cuda")
+    stats = torch.zeros(7, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(D.tdc_workspace_bytes(M, H), dtype=torch.uint8, device="cuda")
+    D.tdc_step_nvfp4(1, xi.cuda(), xo.cuda(), cache, g_new=g_new, amax_out=am, stats_out=stats, workspace=ws)
+    out = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+    D.tdc_step_nvfp4(0, xo.cuda(), out, cache)
+    torch.cuda.synchronize()
+    cn, sn, st, am_ref = orc.block_stats_nvfp4(synth.bits(xi), synth.bits(xo), cp, sp, 0.01, g_new.item())
+    assert np.array_equal(cache.codes.cpu().numpy(), cn) and np.array_equal(cache.sf.cpu().numpy(), sn)
+    assert am.item() == am_ref and cache.g.item() == g_new.item()
+    s = stats.cpu().numpy()
+    np.testing.assert_allclose(s[:4], st[:4], rtol=4.2e-7)
+    np.testing.assert_allclose(s[4:], st[4:], rtol=1e-12)
+    assert np.array_equal(synth.bits(out.cpu()), orc.tdc_skip_nvfp4(synth.bits(xo), cn, sn, g_new.item()))
