@@ -52,6 +52,26 @@ struct SegReduce {
         for (int i = 0; i < nseg; ++i) t = __fadd_rn(t, lds_f32(red + 4u * (slot * MAX_SEG + seg0 + i)));
         return t;
     }
+    // two sums in one barrier (slots `slot` and `slot + 1`)
+    __device__ __forceinline__ void sum2(float& a, float& b, int slot) const {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = __fadd_rn(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if ((threadIdx.x & 15) == 0) {
+            sts_f32(red + 4u * (slot * MAX_SEG + (threadIdx.x >> 4)), a);
+            sts_f32(red + 4u * ((slot + 1) * MAX_SEG + (threadIdx.x >> 4)), b);
+        }
+        __syncthreads();
+        float ta = 0.0f, tb = 0.0f;
+        for (int i = 0; i < nseg; ++i) {
+            ta = __fadd_rn(ta, lds_f32(red + 4u * (slot * MAX_SEG + seg0 + i)));
+            tb = __fadd_rn(tb, lds_f32(red + 4u * ((slot + 1) * MAX_SEG + seg0 + i)));
+        }
+        a = ta;
+        b = tb;
+    }
     __device__ __forceinline__ float max(float v, int slot) const {
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -70,6 +90,11 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, int 
         : "memory");
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -196,21 +221,28 @@ __global__ void __launch_bounds__(MAX_THREADS) quant_tma_kernel(const QuantParam
         }
 
         if (ln) {
-            // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue, R13)
-            f2 s2 = f2make(0.0f, 0.0f);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) s2 = add2(s2, Y[q]);
-            const float mean = __fdiv_rn(sr.sum(__fadd_rn(f2lo(s2), f2hi(s2)), s0 + 0), (float)p.k);
-            const f2 nm = f2make(-mean, -mean);
-            f2 q2 = f2make(0.0f, 0.0f);
+            // h = bf16((x - mean) * (1/sqrt(var + eps))), var = mean((x - mean)^2)  (glue, R13).
+            // One pass and one reduction: sums of d = x - c and d^2 around the row's first
+            // element c (read straight from the staged row), mean = c + S1/k,
+            // var = S2/k - (S1/k)^2 (shifted data keeps the cancellation small).
+            const uint32_t L0 = (uint32_t)(grp * nch);
+            const float c = bf16lo(lds32(sbase + b * set_stride + L0 * 128 + ((0u ^ (L0 & 7)) << 4)));
+            const f2 nc = f2make(-c, -c);
+            f2 s1 = f2make(0.0f, 0.0f), s2 = f2make(0.0f, 0.0f);
             if (cvalid) {
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    const f2 d = add2(Y[q], nm);
-                    q2 = fma2(d, d, q2);
+                    const f2 d = add2(Y[q], nc);
+                    s1 = add2(s1, d);
+                    s2 = fma2(d, d, s2);
                 }
             }
-            const float var = __fdiv_rn(sr.sum(__fadd_rn(f2lo(q2), f2hi(q2)), s0 + 1), (float)p.k);
+            float S1 = __fadd_rn(f2lo(s1), f2hi(s1)), S2 = __fadd_rn(f2lo(s2), f2hi(s2));
+            sr.sum2(S1, S2, s0 + 0);
+            const float md = __fdiv_rn(S1, (float)p.k);
+            const float mean = __fadd_rn(c, md);
+            const f2 nm = f2make(-mean, -mean);
+            const float var = fmaxf(__fsub_rn(__fdiv_rn(S2, (float)p.k), __fmul_rn(md, md)), 0.0f);
             const float rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps)));
             const f2 rs = f2make(rstd, rstd);
 #pragma unroll

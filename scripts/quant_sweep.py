@@ -12,16 +12,17 @@ res = {}
 for k in (3072, 12288):
     xs = [synth.dit_activation(m, k, seed=i).cuda() for i in range(2)]
     g = torch.tensor([1e-3], device="cuda")
-    for fmt in ("nvfp4", "int8"):
+    for fmt in ("nvfp4", "int8", "both"):
         for had in (True, False):
-            a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g) if fmt == "nvfp4" else None
-            a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda") if fmt == "int8" else None
-            for i in range(3):
-                D.dmpq_quantize_act(xs[i % 2], out_fp4=a4, out_i8=a8, hadamard=had)
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize(); s.record()
-            for i in range(20):
-                D.dmpq_quantize_act(xs[i % 2], out_fp4=a4, out_i8=a8, hadamard=had)
-            e.record(); torch.cuda.synchronize()
-            res[f"{k}_{fmt}_{'had' if had else 'plain'}"] = round(s.elapsed_time(e) / 20 * 1e3, 1)
+            a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g) if fmt in ("nvfp4", "both") else None
+            a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda") if fmt in ("int8", "both") else None
+            for ln in ((False, True) if k == 3072 else (False,)):
+                for i in range(3):
+                    D.dmpq_quantize_act(xs[i % 2], out_fp4=a4, out_i8=a8, hadamard=had, layernorm=ln)
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize(); s.record()
+                for i in range(20):
+                    D.dmpq_quantize_act(xs[i % 2], out_fp4=a4, out_i8=a8, hadamard=had, layernorm=ln)
+                e.record(); torch.cuda.synchronize()
+                res[f"{k}_{fmt}_{'had' if had else 'plain'}{'_ln' if ln else ''}"] = round(s.elapsed_time(e) / 20 * 1e3, 1)
 print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("DMPQ_QUANT")}, "us": res}))
