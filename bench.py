@@ -184,6 +184,9 @@ def run_ours(args):
         nb = args.blocks
     r0, r1 = shard_rows(M, world, rank)
     m = r1 - r0
+    if args.rank_share:   # development: one rank's share of an N-GPU run, on one GPU (no exchange)
+        r0, r1 = shard_rows(M, args.rank_share, 0)
+        m = r1 - r0
     T = max(T, args.warmup + args.steps)
     peaks, peak_kind = load_peaks()
 
@@ -442,6 +445,8 @@ def main():
     ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
     ap.add_argument("--pdr", action="store_true", help="enable the Purified Cache Refresh outlier gate (P:241, "
                     "NEXT-3; off by default: the north_star path is DMPQ + TDC)")
+    ap.add_argument("--rank-share", type=int, default=0, help="development: time one rank's token share of an "
+                    "N-GPU run on this GPU (host-overhead study; not a bench line)")
     ap.add_argument("--bounds", action="store_true", help="also time all-NVFP4 and all-INT8 steps without skips "
                     "(SURVEY 8(d) bounds)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
