@@ -1,0 +1,42 @@
+"""Small invocations of every kernel for compute-sanitizer runs (memcheck / racecheck / synccheck)."""
+import sys
+import torch
+sys.path.insert(0, '/root/repo')
+from paper_2603_18742_b200 import build, dmpq as D, synth  # noqa: E402
+build.build()
+dev = "cuda"
+for (m, k) in [(37, 1920), (130, 3072)]:
+    x = synth.dit_activation(m, k, seed=m).to(dev)
+    g = torch.tensor([0.01], device=dev)
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, dev, g=g)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, dev)
+    h = torch.empty(m, k, dtype=torch.bfloat16, device=dev)
+    rs = torch.zeros(m, device=dev)
+    ai = torch.zeros(1, device=dev)
+    for had in (False, True):
+        for ln in (False, True):
+            D.dmpq_quantize_act(x, out_i8=a8, out_fp4=a4, layernorm=ln, h_out=h if ln else None, hadamard=had,
+                                row_abs_sum=rs, amax_in=ai)
+    w, b = synth.linear_weight(256, k, seed=1)
+    for had in (False, True):
+        pw = D.dmpq_pack_weights(w.to(dev), b.to(dev), hadamard=had, keep_bf16=True)
+        y = torch.empty(m, 256, dtype=torch.bfloat16, device=dev)
+        D.dmpq_gemm(a8, pw, Y=y)
+        D.dmpq_gemm(a4, pw, Y=y, gelu=True)
+        D.dmpq_gemm(D.QuantAct.bf16(x), pw, Y=y)
+H = 128
+m = 256
+xi = synth.dit_activation(m, H, seed=1).to(dev)
+xo = synth.dit_activation(m, H, seed=2).to(dev)
+st = torch.zeros(7, dtype=torch.float64, device=dev)
+ws = torch.zeros(D.tdc_workspace_bytes(m, H), dtype=torch.uint8, device=dev)
+delta = torch.zeros(m, H, dtype=torch.bfloat16, device=dev)
+D.tdc_step(1, xi, xo, delta, st, ws)
+D.tdc_step(0, xi, xo, delta)
+cache = D.DeltaCacheNvfp4(m, H, dev)
+am = torch.zeros(1, device=dev)
+D.tdc_delta_amax(xi, xo, am)
+D.tdc_step_nvfp4(1, xi, xo, cache, g_new=torch.tensor([0.01], device=dev), amax_out=am, stats_out=st, workspace=ws)
+D.tdc_step_nvfp4(0, xi, xo, cache)
+torch.cuda.synchronize()
+print("sanitize_small ok")
