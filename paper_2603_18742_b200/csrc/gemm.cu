@@ -69,7 +69,10 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8
 // mainloop of tile i+1). Epilogue: TMEM -> registers -> 64B-swizzled smem staging
 // -> TMA store; per-column vectors (bias, w_scale, gate) staged in smem per tile.
 // ============================================================================
-constexpr int EPI_WARPS = 8;   // epilogue warps per CTA (2 per TMEM lane quarter, column-interleaved)
+#ifndef DMPQ_EPI_WARPS
+#define DMPQ_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = DMPQ_EPI_WARPS;   // epilogue warps per CTA (2 per TMEM lane quarter, column-interleaved)
 
 template <int KIND, int BN, int STAGES>   // KIND: 0 INT8, 1 NVFP4, 2 BF16
 struct PairLayout {
@@ -284,6 +287,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                 if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
             }
             for (int c = chalf; c < nch_here; c += CSTEP) {
+                // gated-residual row chunk: loaded before the TMEM read so the two latencies overlap
+                uint4 rv4[4];
+                if (has_res && row_ok) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + (size_t)row * p.ldr + n0 + c * 32);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4) rv4[v4] = __ldg(rp + v4);
+                }
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
@@ -331,10 +341,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     }
                 }
                 if (has_res && row_ok) {
-                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + (size_t)row * p.ldr + col0);
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
-                        const uint4 rv = rp[v4];
+                        const uint4 rv = rv4[v4];
                         const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
                         float g0, g1, g2, g3, g4, g5, g6, g7;
                         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
