@@ -519,6 +519,7 @@ extern "C" dmpq_status dmpq_prepare(void) {
         if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
     }
     if (rc == DMPQ_OK) rc = prepare_quant_tma();
+    if (rc == DMPQ_OK) rc = prepare_quant_had();
     return rc;
 }
 

@@ -85,6 +85,11 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
     if (m == 0) return DMPQ_OK;
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_quantize_act: needs an sm_100 device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+    if (p.flags & DMPQ_QF_HADAMARD) {
+        // DMPQ_QUANT_HAD_CHUNK=1 selects the previous 64-element-chunk kernel (A/B measurements)
+        static const bool chunk = [] { const char* e = getenv("DMPQ_QUANT_HAD_CHUNK"); return e && e[0] == '1'; }();
+        if (!chunk) return launch_quant_had(p, st);
+    }
     return launch_quant_tma(p, (p.flags & DMPQ_QF_HADAMARD) != 0, st);
 }
 

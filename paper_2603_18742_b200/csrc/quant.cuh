@@ -89,5 +89,8 @@ __device__ __forceinline__ uint32_t int8x4(f2 q01, f2 q23) {
 // Chunk quantizer (quant_tma.cu): rows staged by TMA, 64 elements per thread.
 dmpq_status launch_quant_tma(const QuantParams& p, bool hadamard, cudaStream_t s);
 dmpq_status prepare_quant_tma();
+// Hadamard quantizer (quant_had.cu): one 128-element block per thread, all FHT stages in registers.
+dmpq_status launch_quant_had(const QuantParams& p, cudaStream_t s);
+dmpq_status prepare_quant_had();
 
 }  // namespace dmpq

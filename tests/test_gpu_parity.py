@@ -271,6 +271,31 @@ def test_quantize_hadamard_bit_exact(D, orc, m, k, ln):
     assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
 
 
+@pytest.mark.parametrize("k,ln", [(3072, False), (3072, True), (12288, False)])
+def test_quantize_hadamard_dense_rows(D, orc, k, ln):
+    """Several thousand full rows through the Hadamard quantizer (both formats): enough
+    elements that fl(y r) lands exactly on INT8 / E2M1 rounding ties many times, so a
+    contracted multiply-add (one rounding instead of RNE(fl(y r))) cannot pass."""
+    m = 2053   # ragged: not a multiple of the kernel's rows per CTA
+    x = synth.dit_activation(m, k, seed=k + 17) if k == 3072 else synth.ffn2_activation(m, k, seed=k + 17)
+    h = torch.empty(m, k, dtype=torch.bfloat16, device="cuda") if ln else None
+    g = torch.tensor([0.004], device="cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    amax = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a8, out_fp4=a4, amax_out=amax, layernorm=ln, h_out=h, hadamard=True)
+    torch.cuda.synchronize()
+    src = synth.bits(h.cpu()) if ln else synth.bits(x)
+    y = orc.fht128(orc.bf16_to_f32(src).reshape(m, k))
+    assert amax.item() == float(np.abs(y).max())
+    c8, s8 = orc.int8_quantize_f32(y)
+    assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+    assert np.array_equal(a8.codes.cpu().numpy(), c8)
+    c4, s4 = orc.nvfp4_quantize_f32(y, 0.004)
+    assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s4)
+    assert np.array_equal(a4.codes.cpu().numpy(), c4)
+
+
 @pytest.mark.parametrize("k", [128, 1920])
 def test_quantize_hadamard_adversarial_rows(D, orc, k):
     """The Hadamard quantizer on the adversarial rows (zero, tiny, huge, constant rows,
