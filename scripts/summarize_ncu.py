@@ -38,7 +38,9 @@ def raw(rep):
     return res
 
 
-summary = {}
+# merge: captures present in gpurun_out/ replace their entries, the others are kept
+out_json = os.path.join(DST, "ncu_full_summary.json")
+summary = json.load(open(out_json)) if os.path.exists(out_json) else {}
 for rep in sorted(glob.glob(os.path.join(SRC, "full_*.ncu-rep"))):
     summary[os.path.basename(rep)] = raw(rep)
 json.dump(summary, open(os.path.join(DST, "ncu_full_summary.json"), "w"), indent=1)
