@@ -116,7 +116,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
-    constexpr uint32_t ACC_COLS = 2 * BN;
+    // accumulator buffers in TMEM: two (the epilogue of tile i overlaps the mainloop of tile
+    // i + 1) unless BN = 256 NVFP4, where 2 x 256 columns leave no room for the scale factors:
+    // one buffer, and the mainloop of tile i + 1 waits for the epilogue of tile i
+    constexpr int NACC = (FP4 && BN == 256) ? 1 : 2;
+    constexpr uint32_t ACC_COLS = NACC * BN;
     constexpr uint32_t SF_COLS = FP4 ? (4 * 4 + 4 * 8) : 0;
     static_assert(ACC_COLS + SF_COLS <= 512, "TMEM budget");
     constexpr uint32_t TMEM_COLS = 512;
@@ -191,8 +195,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                 // SFB rows start at the 128-row atom below n0; BN=192 odd tiles start 64 rows (2 columns) in
                 const uint32_t sfb_shift = (uint32_t)(((nt * BN) & 127) >> 5);
                 mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);
+                if constexpr (NACC == 1) {   // single buffer: the previous tile's epilogue must be done too
+                    if (local >= 1) mbar_wait(bar_tempty + 8 * ((local - 1) & 1), ((local - 1) >> 1) & 1);
+                }
                 tc_fence_after();
-                const uint32_t d_t = tmem_base + acc * BN;
+                const uint32_t d_t = tmem_base + (NACC == 2 ? acc * BN : 0);
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(bar_full + 8 * stage, phase);
                     tc_fence_after();
@@ -295,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     for (int v4 = 0; v4 < 4; ++v4) rv4[v4] = __ldg(rp + v4);
                 }
                 uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (NACC == 2 ? acc * BN : 0) + c * 32, r);
                 tmem_ld_wait();
                 if (c == my_last) {   // this warp's last TMEM read of the accumulator
                     tc_fence_before();
@@ -506,6 +513,15 @@ static int gemm_stages() {
     return st;
 }
 
+// NVFP4 tile width (experiment knob DMPQ_FP4_BN = 192 | 256; 256 = single-buffered accumulator).
+static int fp4_bn() {
+    static int bn = [] {
+        const char* e = std::getenv("DMPQ_FP4_BN");
+        return (e && std::atoi(e) == 256) ? 256 : 192;
+    }();
+    return bn;
+}
+
 extern "C" dmpq_status dmpq_prepare(void) {
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_prepare: needs an sm_100 device");
     dmpq_status rc = DMPQ_OK;
@@ -518,6 +534,7 @@ extern "C" dmpq_status dmpq_prepare(void) {
         if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 6>();
         if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
     }
+    if (rc == DMPQ_OK && fp4_bn() == 256) rc = set_pair_attrs<1, 256, 5>();
     if (rc == DMPQ_OK) rc = prepare_quant_tma();
     if (rc == DMPQ_OK) rc = prepare_quant_had();
     return rc;
@@ -561,6 +578,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
+        if (fp4_bn() == 256) return launch_gemm_pair<1, 256, 5>(p, A->codes, W->fp4_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st)
                                  : launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
     } else if (A->fmt == DMPQ_FMT_BF16) {
