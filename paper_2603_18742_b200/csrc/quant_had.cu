@@ -134,7 +134,7 @@ __device__ __forceinline__ uint32_t int8x4_magic(f2 y01, f2 y23, f2 r2, f2 z2) {
 #ifndef DMPQ_HAD_LN_MINB
 #define DMPQ_HAD_LN_MINB 3   // CTAs per SM the LN variant is register-limited for (experiments)
 #endif
-template <bool LN, bool PDR>
+template <bool LN, bool PDR, bool WH>   // WH: write h (LN variants only)
 __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_kernel(const QuantParams p, const __grid_constant__ CUtensorMap tmX,
                                                               int tpr, int R, int set_stride, int nbuf, int split) {
     extern __shared__ uint8_t hsm_raw[];
@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
     const uint32_t tx_bytes = (uint32_t)(R * nb * 256);
     const Seg8 sr{red, grp * (tpr >> 3), tpr >> 3};
     const bool want_fp4 = p.fp4_codes != nullptr, want_i8 = p.i8_codes != nullptr;
-    const bool write_h = (p.flags & DMPQ_QF_WRITE_H) != 0;
     constexpr bool pdr = PDR;   // p.row_abs_sum or p.amax_in requested
 
     // NVFP4 block-scale constants: raw = fl(fl(a/6)/g) takes the exact fast division when g is
@@ -270,7 +269,7 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
                     }
                     Y[q] = fma2(f2make(bb, bb), pm, f2make(a, a));
                 }
-                if (write_h && live) {
+                if (WH && live) {
                     uint32_t w[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
@@ -439,7 +438,7 @@ int had_ctas_per_sm(int threads, int smem) {
     for (int i = 0; i < 8; ++i)
         if (cache_threads[i] == threads && cache_smem[i] == smem) return cache_n[i];
     int n = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quant_had_kernel<false, false>, threads, smem) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quant_had_kernel<false, false, false>, threads, smem) != cudaSuccess || n < 1) {
         cudaGetLastError();
         n = 1;
     }
@@ -451,10 +450,13 @@ int had_ctas_per_sm(int threads, int smem) {
 }  // namespace
 
 dmpq_status prepare_quant_had() {
-    if (cudaFuncSetAttribute(quant_had_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(quant_had_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(quant_had_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(quant_had_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) != cudaSuccess)
+    const void* kernels[] = {(const void*)quant_had_kernel<false, false, false>, (const void*)quant_had_kernel<true, false, false>,
+                             (const void*)quant_had_kernel<true, false, true>,   (const void*)quant_had_kernel<false, true, false>,
+                             (const void*)quant_had_kernel<true, true, false>,   (const void*)quant_had_kernel<true, true, true>};
+    bool ok = true;
+    for (const void* k : kernels)
+        ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) == cudaSuccess;
+    if (!ok)
         return check_launch("dmpq_quantize_act(smem attribute)");
     return DMPQ_OK;
 }
@@ -488,10 +490,13 @@ dmpq_status launch_quant_had(const QuantParams& p, cudaStream_t s) {
     const int nsets = (p.m + R - 1) / R;
     const int grid = std::max(1, std::min(nsets, had_ctas_per_sm(threads, smem) * num_sms()));
     const bool ln = (p.flags & DMPQ_QF_LAYERNORM) != 0, pdr = p.row_abs_sum != nullptr || p.amax_in != nullptr;
-    if (ln && pdr) quant_had_kernel<true, true><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split);
-    else if (ln) quant_had_kernel<true, false><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split);
-    else if (pdr) quant_had_kernel<false, true><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split);
-    else quant_had_kernel<false, false><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split);
+    const bool wh = ln && (p.flags & DMPQ_QF_WRITE_H) != 0;
+#define DMPQ_HAD_LAUNCH(a, b, c) quant_had_kernel<a, b, c><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split)
+    if (ln && pdr) { if (wh) DMPQ_HAD_LAUNCH(true, true, true); else DMPQ_HAD_LAUNCH(true, true, false); }
+    else if (ln) { if (wh) DMPQ_HAD_LAUNCH(true, false, true); else DMPQ_HAD_LAUNCH(true, false, false); }
+    else if (pdr) DMPQ_HAD_LAUNCH(false, true, false);
+    else DMPQ_HAD_LAUNCH(false, false, false);
+#undef DMPQ_HAD_LAUNCH
     return check_launch("dmpq_quantize_act");
 }
 
