@@ -191,7 +191,7 @@ def run_ours(args):
     peaks, peak_kind = load_peaks()
 
     model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
-                     pdr=args.pdr, m_total=M, cache_nvfp4=args.cache_nvfp4)
+                     pdr=args.pdr, m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh)
     # block-0 input trajectory basis (this rank's rows)
     A, B = synth.trajectory_basis(m, H, seed=1000 + rank, device=dev)
 
@@ -406,7 +406,7 @@ def run_ours(args):
         "config": {"workload": desc, "blocks": nb, "hidden": H, "ffn": F, "tokens_total": M, "tokens_per_rank": m,
                    "timesteps": list(range(args.warmup, args.warmup + args.steps)), "T": T,
                    "parallelism": f"token-shard x{world}", "l2": "inputs larger than L2 (multi-GB working set per step)",
-                   "cuda_graphs": not args.no_graphs,
+                   "cuda_graphs": not args.no_graphs, "tdc_refresh": "fused in the FFN2 GEMM epilogue" if model.fuse_refresh else "own kernel",
                    "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr,
                    "delta_cache": {"format": "nvfp4" if args.cache_nvfp4 else "bf16",
                                    "bytes_per_rank": sum(d.nbytes() if args.cache_nvfp4 else d.numel() * 2
@@ -449,6 +449,8 @@ def main():
                     "N-GPU run on this GPU (host-overhead study; not a bench line)")
     ap.add_argument("--bounds", action="store_true", help="also time all-NVFP4 and all-INT8 steps without skips "
                     "(SURVEY 8(d) bounds)")
+    ap.add_argument("--fused-refresh", action="store_true", help="run the TDC refresh in the FFN2 GEMM epilogue "
+                    "instead of its own kernel (SURVEY NEXT-2; measured slower, DESIGN.md 5.7c)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
     args = ap.parse_args()
     if args.warmup < 3:

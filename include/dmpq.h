@@ -223,13 +223,30 @@ dmpq_status dmpq_global_scale(const float* amax, float div, float* g_out, int co
 #define DMPQ_EP_BIAS      1u  /* + bias[n] (W->bias)                                   */
 #define DMPQ_EP_GELU_TANH 2u  /* y = gelu_tanh(y)  (block glue)                        */
 #define DMPQ_EP_RESIDUAL  4u  /* y = residual[m,n] + gate[n] * y (gated residual glue) */
+#define DMPQ_EP_TDC_REFRESH 8u /* fused TDC refresh of the stored bf16 Y (= X_out), below */
 
 typedef struct {
     uint32_t flags;
     const float* gate;         /* [n] (DMPQ_EP_RESIDUAL) */
     const uint16_t* residual;  /* bf16 [m x n], row stride ldr (DMPQ_EP_RESIDUAL); may alias Y */
     int ldr;
+    /* DMPQ_EP_TDC_REFRESH: tdc_step(TDC_REFRESH, tdc_x_in, Y, tdc_delta, m, n, ...) fused into
+     * the epilogue of the GEMM that produces the block output X_out = Y (Eq. 8; SURVEY
+     * NEXT-2): Delta_new = bf16(fl(bf16(y) - x_in)) overwrites tdc_delta (Delta_prev on entry)
+     * and tdc_stats[0..7) receives the seven dmpq_block_stats sums over the m x n elements, with
+     * tdc_step's arithmetic (FP32 per 8-element vector, then FP64; cosine sums exact products in
+     * FP64) in a fixed order for a given grid (deterministic; not the same order as tdc_step).
+     * Needs the bf16 output Y; tdc_x_in and tdc_delta are dense (row stride n); neither may
+     * alias Y or the residual. tdc_workspace: device, dmpq_gemm_tdc_workspace_bytes() bytes,
+     * zero-filled once before first use (the kernel leaves it ready for the next call). */
+    const uint16_t* tdc_x_in;
+    uint16_t* tdc_delta;
+    double* tdc_stats;
+    void* tdc_workspace;
 } dmpq_epilogue;
+
+/* Workspace bytes of the fused TDC refresh (DMPQ_EP_TDC_REFRESH) on the current device. */
+size_t dmpq_gemm_tdc_workspace_bytes(void);
 
 /* Y = A @ W^T with the dequant/bias epilogue (north_star), on tcgen05.
  *  BF16  (kind::f16, R15): acc = sum_k a*w in the tensor core's FP32 accumulator;

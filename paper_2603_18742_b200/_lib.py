@@ -21,7 +21,7 @@ STATUS_NAMES = ["DMPQ_OK", "DMPQ_EINVAL", "DMPQ_ESHAPE", "DMPQ_EALIGN", "DMPQ_EZ
 FMT_INT8, FMT_NVFP4, FMT_BF16 = 0, 1, 2
 QF_LAYERNORM, QF_WRITE_H, QF_HADAMARD = 1, 2, 4
 PACK_HADAMARD = 1
-EP_BIAS, EP_GELU_TANH, EP_RESIDUAL = 1, 2, 4
+EP_BIAS, EP_GELU_TANH, EP_RESIDUAL, EP_TDC_REFRESH = 1, 2, 4, 8
 TDC_SKIP, TDC_REFRESH = 0, 1
 TDC_COMPUTE, TDC_DECIDE_SKIP = 0, 1
 GAMMA_L1, GAMMA_L2 = 0, 1
@@ -44,7 +44,8 @@ class QuantOpts(ctypes.Structure):
 
 
 class Epilogue(ctypes.Structure):
-    _fields_ = [("flags", c_uint32), ("gate", c_void_p), ("residual", c_void_p), ("ldr", c_int)]
+    _fields_ = [("flags", c_uint32), ("gate", c_void_p), ("residual", c_void_p), ("ldr", c_int),
+                ("tdc_x_in", c_void_p), ("tdc_delta", c_void_p), ("tdc_stats", c_void_p), ("tdc_workspace", c_void_p)]
 
 
 class BlockStats(ctypes.Structure):
@@ -78,6 +79,7 @@ _SIGNATURES = {
     "dmpq_prepare": ([], c_int),
     "dmpq_sf_bytes": ([c_int, c_int], c_size_t),
     "tdc_workspace_bytes": ([c_int, c_int], c_size_t),
+    "dmpq_gemm_tdc_workspace_bytes": ([], c_size_t),
     "dmpq_pack_weights": ([c_void_p, c_int, c_int, ctypes.POINTER(Weights), c_void_p], c_int),
     "dmpq_pack_weights_ex": ([c_void_p, c_int, c_int, c_uint32, ctypes.POINTER(Weights), c_void_p], c_int),
     "dmpq_derive_tau": ([c_double, c_double, c_double, c_double], c_double),

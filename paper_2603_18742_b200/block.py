@@ -92,6 +92,8 @@ class Workspace:
             self.acts[(slot, D.FMT_INT8)] = D.QuantAct.empty(D.FMT_INT8, m, k, device)
             self.acts[(slot, D.FMT_NVFP4)] = D.QuantAct.empty(D.FMT_NVFP4, m, k, device, g=g_table[0, slot:slot + 1])
         self.tdc_ws = torch.zeros(D.tdc_workspace_bytes(m, H), dtype=torch.uint8, device=device)
+        # fused refresh in the FFN2 epilogue (zero-filled once; the kernel resets its counter)
+        self.tdc_gemm_ws = torch.zeros(D.dmpq_gemm_tdc_workspace_bytes(), dtype=torch.uint8, device=device)
         self.h1 = torch.empty(m, H, **e)          # LN outputs, materialised only for BF16-routed layers (R15)
         self.h2 = torch.empty(m, H, **e)
 
@@ -119,7 +121,8 @@ class DiTStack:
     def __init__(self, n_blocks: int, H: int, F: int, m_local: int, device, seed: int = 0,
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
-                 tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False):
+                 tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False,
+                 fuse_refresh: bool = False):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -131,6 +134,9 @@ class DiTStack:
         self.pdr = pdr                # Purified Cache Refresh outlier gate (R15)
         self.tau_outlier = tau_outlier
         self.cache_nvfp4 = cache_nvfp4  # NVFP4-compressed delta cache (R16)
+        # bf16 cache, optional: the TDC refresh runs in the FFN2 GEMM's epilogue (
+        # measured slower than the streaming refresh kernel)
+        self.fuse_refresh = fuse_refresh and not cache_nvfp4
         self.m_total = m_total if m_total is not None else m_local
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
@@ -228,7 +234,7 @@ class DiTStack:
             out[D.FMT_BF16] = D.QuantAct.bf16(h_buf if layernorm else src)
         return out
 
-    def _compute_block(self, b: int, x_in: torch.Tensor, x_out: torch.Tensor, fmts) -> float:
+    def _compute_block(self, b: int, x_in: torch.Tensor, x_out: torch.Tensor, fmts, refresh_stats=None) -> float:
         W, ws, H, F, m = self.blocks[b], self.ws, self.H, self.F, self.m
         cap = self.capture is not None
         # attention input: LN fused into the quantizer, one pass for every format Q/K/V need
@@ -256,7 +262,10 @@ class DiTStack:
         q3 = self._quant(b, 3, ws.f, {fmts[5]})
         if fmts[5] != D.FMT_BF16:
             self._cap_act("a3", q3[fmts[5]])
-        self._gemm(q3[fmts[5]], W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
+        tdc = {}
+        if refresh_stats is not None:   # fused TDC refresh of X_out (Eq. 8) in this epilogue
+            tdc = dict(tdc_x_in=x_in, tdc_delta=self.delta[b], tdc_stats=refresh_stats, tdc_workspace=ws.tdc_gemm_ws)
+        self._gemm(q3[fmts[5]], W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2, **tdc)
         self._cap("x_out", x_out)
         return 2.0 * m * (4 * H * H + 2 * H * F)
 
@@ -310,9 +319,11 @@ class DiTStack:
                 else:
                     D.tdc_step(L.TDC_SKIP, x_in, x_out, self.delta[b])
             return 0.0
+        st = self.stats_slots[self.rank, b, :L.STATS_LEN]
+        if self.fuse_refresh:
+            return self._compute_block(b, x_in, x_out, fmts, refresh_stats=st)
         flops = self._compute_block(b, x_in, x_out, fmts)
         with self._ev("tdc"):
-            st = self.stats_slots[self.rank, b, :L.STATS_LEN]
             if self.cache_nvfp4:
                 am, g = self.delta_amax[b:b + 1], self.g_delta[b:b + 1]
                 am.zero_()
@@ -369,7 +380,7 @@ class DiTStack:
                 flops = 0.0 if d == L.TDC_DECIDE_SKIP else 2.0 * self.m * (4 * self.H * self.H + 2 * self.H * self.F)
             else:
                 flops = self._block_work(b, x_in, x_out, d, fmts, first)
-            self.launches += 1 if d == L.TDC_DECIDE_SKIP else (13 if first else 11)
+            self.launches += 1 if d == L.TDC_DECIDE_SKIP else (13 if first else (10 if self.fuse_refresh else 11))
             rec.linear_flops += flops
             rec.fmts.append(None if d == L.TDC_DECIDE_SKIP else fmts)
             rec.gammas.append(gamma)

@@ -53,6 +53,12 @@ struct GemmParams {
     int ldy;
     float* Y32;
     int32_t* acc_out;
+    // fused TDC refresh (DMPQ_EP_TDC_REFRESH)
+    const uint16_t* tdc_x_in;
+    uint16_t* tdc_delta;
+    double* tdc_stats;
+    double* tdc_partials;      // [gridDim.x * EPI_WARPS][7]
+    unsigned int* tdc_counter;
 };
 
 constexpr int BM = 128;
@@ -259,6 +265,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0;
         const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
         const bool has_res = (p.flags & DMPQ_EP_RESIDUAL) != 0;
+        const bool has_tdc = (p.flags & DMPQ_EP_TDC_REFRESH) != 0;
+        // fused TDC refresh statistics of this warp's rows / chunks over all its tiles (fixed order)
+        double tacc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
             const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int acc = local & 1;
@@ -280,6 +289,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             const int rowbase = mt * 256 + (int)rank * BM + q * 32;
             const int row = rowbase + lane;
             const bool row_ok = row < p.m;
+            if ((has_res || has_tdc) && row_ok && chalf == 0) {
+                // this tile's row segments of the epilogue's global inputs -> L2 while the
+                // mainloop still runs (one bulk prefetch per row and tensor)
+                const uint32_t seg = (uint32_t)min(BN, p.n - n0) * 2;
+                if (has_res) bulk_prefetch_l2(p.residual + (size_t)row * p.ldr + n0, seg);
+                if (has_tdc) {
+                    bulk_prefetch_l2(p.tdc_x_in + (size_t)row * p.n + n0, seg);
+                    bulk_prefetch_l2(p.tdc_delta + (size_t)row * p.n + n0, seg);
+                }
+            }
             float sa = 0.0f;
             if constexpr (I8) sa = row_ok ? p.a_scale[row] : 0.0f;
             const f2 sa2 = f2make(sa, sa);
@@ -363,6 +382,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                             y[v4 * 4 + j] = fma2(gp[j], y[v4 * 4 + j], f2make(bf16lo(w[j]), bf16hi(w[j])));
                     }
                 }
+                uint32_t yb[16];   // the stored bf16 output (X_out for the fused TDC refresh)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) yb[j] = pack_bf16x2_f2(y[j]);
                 if (p.Y) {
                     const uint32_t buf = staging + (L::STAGING_BUFS == 2 ? (chunk_ctr & 1) * 2048 : 0);
                     if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
@@ -373,9 +395,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
                         const uint32_t a = buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);  // 64B swizzle
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pack_bf16x2_f2(y[4 * v4])),
-                                     "r"(pack_bf16x2_f2(y[4 * v4 + 1])), "r"(pack_bf16x2_f2(y[4 * v4 + 2])),
-                                     "r"(pack_bf16x2_f2(y[4 * v4 + 3]))
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(yb[4 * v4]),
+                                     "r"(yb[4 * v4 + 1]), "r"(yb[4 * v4 + 2]), "r"(yb[4 * v4 + 3])
                                      : "memory");
                     }
                     fence_proxy_async_smem();
@@ -385,6 +406,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                         bulk_commit();
                     }
                     ++chunk_ctr;
+                }
+                if (has_tdc && row_ok) {
+                    // TDC refresh (Eq. 8) with tdc_step's arithmetic: d = fl(X_out - X_in),
+                    // Delta_new = bf16(d); Gamma / L2 sums FP32 per 8-element vector then FP64,
+                    // cosine sums exact bf16 products in FP64 (R12)
+                    const size_t off = (size_t)row * p.n + col0;
+                    const uint4* xp = reinterpret_cast<const uint4*>(p.tdc_x_in + off);
+                    uint4* dp = reinterpret_cast<uint4*>(p.tdc_delta + off);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const uint4 xv = __ldg(xp + v), pv = dp[v];
+                        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
+                        float sv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                        uint32_t o[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t yw = yb[4 * v + j];
+                            const float xa = bf16lo(xw[j]), xb = bf16hi(xw[j]);
+                            const float da = __fsub_rn(bf16lo(yw), xa), db = __fsub_rn(bf16hi(yw), xb);
+                            o[j] = pack_bf16x2(da, db);
+                            const double na = (double)bf16lo(o[j]), nb = (double)bf16hi(o[j]);
+                            const double pa = (double)bf16lo(pw[j]), pb = (double)bf16hi(pw[j]);
+                            sv[0] = __fadd_rn(sv[0], __fadd_rn(fabsf(da), fabsf(db)));
+                            sv[1] = __fadd_rn(sv[1], __fadd_rn(fabsf(xa), fabsf(xb)));
+                            sv[2] = __fadd_rn(sv[2], __fadd_rn(__fmul_rn(da, da), __fmul_rn(db, db)));
+                            sv[3] = __fadd_rn(sv[3], __fadd_rn(__fmul_rn(xa, xa), __fmul_rn(xb, xb)));
+                            tacc[4] = __fma_rn(na, pa, tacc[4]); tacc[4] = __fma_rn(nb, pb, tacc[4]);
+                            tacc[5] = __fma_rn(na, na, tacc[5]); tacc[5] = __fma_rn(nb, nb, tacc[5]);
+                            tacc[6] = __fma_rn(pa, pa, tacc[6]); tacc[6] = __fma_rn(pb, pb, tacc[6]);
+                        }
+                        dp[v] = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) tacc[j] = __dadd_rn(tacc[j], (double)sv[j]);
+                    }
                 }
                 if (row_ok) {
                     if (p.Y32) {
@@ -401,6 +456,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                                 ap[v4] = make_int4((int)r[4 * v4], (int)r[4 * v4 + 1], (int)r[4 * v4 + 2], (int)r[4 * v4 + 3]);
                         }
                     }
+                }
+            }
+        }
+        if (has_tdc) {
+            // per-warp partial (fixed butterfly), then the last warp of the grid sums the
+            // partials in slot order: deterministic for a given grid
+#pragma unroll
+            for (int j = 0; j < 7; ++j) tacc[j] = warp_sum_d(tacc[j]);
+            const int nslots = (int)gridDim.x * EPI_WARPS;
+            const int slot = (int)blockIdx.x * EPI_WARPS + ew;
+            unsigned int last = 0;
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j < 7; ++j) p.tdc_partials[(size_t)slot * 7 + j] = tacc[j];
+                __threadfence();
+                last = (atomicAdd(p.tdc_counter, 1u) == (unsigned)nslots - 1u) ? 1u : 0u;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence();
+                double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                for (int i = lane; i < nslots; i += 32)
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) v[j] = __dadd_rn(v[j], __ldcg(p.tdc_partials + (size_t)i * 7 + j));
+#pragma unroll
+                for (int j = 0; j < 7; ++j) v[j] = warp_sum_d(v[j]);
+                if (lane == 0) {
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) p.tdc_stats[j] = v[j];
+                    *p.tdc_counter = 0u;   // ready for the next call
                 }
             }
         }
@@ -513,6 +598,10 @@ static int gemm_stages() {
     return st;
 }
 
+// fused TDC refresh workspace: partials of up to 1024 CTAs x EPI_WARPS warps, then the counter
+constexpr size_t kTdcPartialBytes = (size_t)1024 * EPI_WARPS * 7 * sizeof(double);
+extern "C" size_t dmpq_gemm_tdc_workspace_bytes(void) { return kTdcPartialBytes + 256; }
+
 // NVFP4 tile width (experiment knob DMPQ_FP4_BN = 192 | 256; 256 = single-buffered accumulator).
 static int fp4_bn() {
     static int bn = [] {
@@ -566,8 +655,22 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
                      "dmpq_gemm: residual/gate");
         p.gate = ep->gate; p.residual = ep->residual; p.ldr = ep->ldr;
     }
+    if (p.flags & DMPQ_EP_TDC_REFRESH) {
+        DMPQ_REQUIRE(Y && ep->tdc_x_in && ep->tdc_delta && ep->tdc_stats && ep->tdc_workspace && aligned16(ep->tdc_x_in) &&
+                         aligned16(ep->tdc_delta) && aligned16(ep->tdc_workspace),
+                     DMPQ_EALIGN, "dmpq_gemm: DMPQ_EP_TDC_REFRESH needs Y and 16-byte aligned tdc_x_in / tdc_delta / workspace");
+        p.tdc_x_in = ep->tdc_x_in; p.tdc_delta = ep->tdc_delta; p.tdc_stats = ep->tdc_stats;
+        p.tdc_partials = reinterpret_cast<double*>(ep->tdc_workspace);
+        p.tdc_counter = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(ep->tdc_workspace) + kTdcPartialBytes);
+    }
     p.Y = Y; p.ldy = ldy; p.Y32 = Y32; p.acc_out = acc_or_null;
-    if (m == 0) return DMPQ_OK;
+    if (m == 0) {
+        if (p.flags & DMPQ_EP_TDC_REFRESH) {   // empty sums
+            if (cudaMemsetAsync(ep->tdc_stats, 0, 7 * sizeof(double), reinterpret_cast<cudaStream_t>(s)) != cudaSuccess)
+                return check_launch("dmpq_gemm(empty TDC stats)");
+        }
+        return DMPQ_OK;
+    }
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_gemm: needs an sm_100 device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
     if (fp4) {

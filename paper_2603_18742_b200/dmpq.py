@@ -197,21 +197,32 @@ def dmpq_global_scale(amax: torch.Tensor, div: float, g_out: torch.Tensor):
 
 def dmpq_gemm(A: QuantAct, W: PackedWeights, Y: torch.Tensor | None = None, Y32: torch.Tensor | None = None,
               acc: torch.Tensor | None = None, bias: bool = True, gelu: bool = False,
-              residual: torch.Tensor | None = None, gate: torch.Tensor | None = None):
-    """Y = epilogue(A @ W^T) on tcgen05 (kind::i8 or kind::mxf4nvf4)."""
+              residual: torch.Tensor | None = None, gate: torch.Tensor | None = None,
+              tdc_x_in: torch.Tensor | None = None, tdc_delta: torch.Tensor | None = None,
+              tdc_stats: torch.Tensor | None = None, tdc_workspace: torch.Tensor | None = None):
+    """Y = epilogue(A @ W^T) on tcgen05 (kind::i8 or kind::mxf4nvf4). With tdc_x_in / tdc_delta /
+    tdc_stats / tdc_workspace the epilogue also runs the TDC refresh of X_out = Y (fused tdc_step)."""
     flags = (L.EP_BIAS if (bias and W.bias is not None) else 0) | (L.EP_GELU_TANH if gelu else 0)
-    ep = None
     if residual is not None:
         flags |= L.EP_RESIDUAL
-        ep = L.Epilogue(flags, gate.data_ptr(), residual.data_ptr(), residual.stride(0))
-    elif flags:
-        ep = L.Epilogue(flags, None, None, 0)
+    if tdc_x_in is not None:
+        flags |= L.EP_TDC_REFRESH
+        for t_, n_ in ((tdc_x_in, "tdc_x_in"), (tdc_delta, "tdc_delta")):
+            _check_dev(t_, n_, torch.bfloat16)
+    ep = None
+    if flags:
+        ep = L.Epilogue(flags, _ptr(gate), _ptr(residual), 0 if residual is None else residual.stride(0),
+                        _ptr(tdc_x_in), _ptr(tdc_delta), _ptr(tdc_stats), _ptr(tdc_workspace))
     if Y is not None:
         _check_dev(Y, "Y", torch.bfloat16)
     L.check("dmpq_gemm", L.lib().dmpq_gemm(
         ctypes.byref(A.c), ctypes.byref(W.c), None if ep is None else ctypes.byref(ep), _ptr(Y),
         0 if Y is None else Y.stride(0), _ptr(Y32), _ptr(acc), _stream(A.codes.device)))
     return Y
+
+
+def dmpq_gemm_tdc_workspace_bytes() -> int:
+    return int(L.lib().dmpq_gemm_tdc_workspace_bytes())
 
 
 # --------------------------------------------------------------------------- predictor (host-pure)

@@ -37,8 +37,9 @@ def close_bf16(gpu_bf16, ref64, rel=2.0 ** -7):
 
 
 MODES = {
-    # name: (hadamard, pdr, tau_outlier, NVFP4-compressed delta cache, TDC tau)
+    # name: (hadamard, pdr, tau_outlier, NVFP4-compressed delta cache, TDC tau[, refresh fused in the FFN2 epilogue])
     "dmpq_tdc": (False, False, 25.0, False, 0.003),
+    "dmpq_tdc_fused_refresh": (False, False, 25.0, False, 0.003, True),
     "hadamard_pdr": (True, True, 9.0, False, 0.003),   # tau_outlier between the O-input and FFN2-input ratios: mixed BF16
     # the compressed cache's quantization noise enters Eq. 9 (E >= ~eps^2/2 ~ 0.004 here, R16): a looser tau
     # so that the trajectory still skips
@@ -62,10 +63,11 @@ def run(request):
     build.build()
     dev = torch.device("cuda")
     M, H, F, T = 256, 128, 512, 6
-    had, pdr, tau_o, c4, tau_c = MODES[request.param]
+    had, pdr, tau_o, c4, tau_c = MODES[request.param][:5]
+    fused = len(MODES[request.param]) > 5 and MODES[request.param][5]
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
     stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o,
-                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2))
+                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused)
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):

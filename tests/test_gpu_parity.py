@@ -172,6 +172,47 @@ def test_gemm_nvfp4_rel_l2(D, orc, m, n, k):
     assert torch.equal(y.cpu(), y32.cpu().to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("fmt,m,n,k", [(0, 300, 512, 256), (1, 300, 512, 256), (0, 1029, 1920, 512),
+                                       (1, 1029, 1920, 512), (2, 257, 384, 128), (1, 1, 256, 128)])
+def test_gemm_fused_tdc_refresh(D, orc, fmt, m, n, k):
+    """TDC refresh fused into the gated-residual GEMM epilogue (DMPQ_EP_TDC_REFRESH, SURVEY
+    NEXT-2): Y equals the unfused GEMM's Y, Delta_new = bf16(Y - X_in) bit-exact, the seven
+    statistics within tdc_step's bounds of the oracle, deterministic run to run."""
+    x = synth.dit_activation(max(m, 1), k, seed=m + k + 5)[:m]
+    w, b = synth.linear_weight(n, k, seed=n + 7)
+    pw = D.dmpq_pack_weights(w.cuda(), b, keep_bf16=(fmt == 2))
+    g = torch.tensor([0.01], device="cuda")
+    if fmt == 2:
+        a = D.QuantAct.bf16(x.cuda())
+    else:
+        a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == 1 else None)
+        D.dmpq_quantize_act(x.cuda(), out_fp4=a if fmt == 1 else None, out_i8=a if fmt == 0 else None)
+    act = lambda s_: synth.dit_activation(max(m, 1), n, seed=s_, outlier_frac=0, tail_frac=0)[:m]
+    res, xin = act(m + 11).cuda(), act(m + 12).cuda()
+    dp = (0.05 * act(m + 13).float()).to(torch.bfloat16)
+    gate = (0.01 * torch.rand(n, generator=torch.Generator().manual_seed(n))).cuda()
+    y_ref = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y_ref, residual=res, gate=gate)
+    ws = torch.zeros(D.dmpq_gemm_tdc_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+        delta = dp.cuda().clone()
+        stats = torch.full((7,), -1.0, dtype=torch.float64, device="cuda")
+        D.dmpq_gemm(a, pw, Y=y, residual=res, gate=gate, tdc_x_in=xin, tdc_delta=delta, tdc_stats=stats,
+                    tdc_workspace=ws)
+        torch.cuda.synchronize()
+        outs.append((y.cpu(), delta.cpu(), stats.cpu()))
+    y, delta, stats = outs[0]
+    assert torch.equal(y, y_ref.cpu())
+    dn_ref, st_ref = orc.block_stats(_u16(xin.cpu()), _u16(y), _u16(dp))
+    assert np.array_equal(synth.bits(delta), dn_ref)
+    st = stats.numpy()
+    np.testing.assert_allclose(st[:4], st_ref[:4], rtol=4.2e-7, atol=0)
+    np.testing.assert_allclose(st[4:], st_ref[4:], rtol=1e-12, atol=1e-300)
+    assert torch.equal(outs[1][1], delta) and torch.equal(outs[1][2], stats)
+
+
 @pytest.mark.parametrize("m,h", [(1, 8), (256, 128), (1000, 1920), (777, 3072)])
 def test_tdc_refresh_and_skip(D, orc, m, h):
     xi = synth.dit_activation(m, h, seed=m + 1, outlier_frac=0, tail_frac=0)
