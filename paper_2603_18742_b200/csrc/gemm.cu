@@ -94,20 +94,21 @@ struct PairLayout {
     static constexpr int SMEM_LIMIT = 232448;                     // 227 KB opt-in per CTA
     // double-buffered output staging when it fits next to the stage ring, else single-buffered
     static constexpr int STAGING_BUFS =
-        (STAGING_OFFSET + EPI_WARPS * 2 * 2048 + VEC_BYTES + 256 + 1024 <= SMEM_LIMIT) ? 2 : 1;
+        (STAGING_OFFSET + EPI_WARPS * 2 * 2048 + VEC_BYTES + 512 + 1024 <= SMEM_LIMIT) ? 2 : 1;
     static constexpr int STAGING_BYTES = EPI_WARPS * STAGING_BUFS * 2048;
     static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
     static constexpr int BAR_OFFSET = VEC_OFFSET + VEC_BYTES;
-    static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;
+    static constexpr int TOTAL = BAR_OFFSET + 512 + 1024;   // mbarriers, TMEM holder, residual barriers
     static_assert(STAGE_BYTES % 1024 == 0, "stage buffers must stay 1024-B aligned");
     static_assert(TOTAL <= SMEM_LIMIT, "shared memory budget");
 };
 
-template <int KIND, int BN, int STAGES>
+template <int KIND, int BN, int STAGES, bool TDC = false>   // TDC: fused refresh epilogue compiled in
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     dmpq_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
-                          const __grid_constant__ CUtensorMap tmY, const GemmParams p) {
+                          const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
+                          const GemmParams p) {
     using L = PairLayout<KIND, BN, STAGES>;
     constexpr bool FP4 = KIND == 1;
     constexpr bool I8 = KIND == 0;
@@ -119,6 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     const uint32_t bar_tfull = bar_empty + STAGES * 8;
     const uint32_t bar_tempty = bar_tfull + 2 * 8;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFFSET + 2 * STAGES * 8 + 4 * 8);
+    const uint32_t bar_res = bar_full + 2 * STAGES * 8 + 4 * 8 + 16;   // [EPI_WARPS][2] residual-chunk TMA loads
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -136,6 +138,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         prefetch_tmap(&tmB);
         if constexpr (FP4) { prefetch_tmap(&tmSFA); prefetch_tmap(&tmSFB); }
         if (p.Y) prefetch_tmap(&tmY);
+        if (p.Y && (p.flags & DMPQ_EP_RESIDUAL)) prefetch_tmap(&tmR);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(bar_full + 8 * s, 1);
             mbar_init(bar_empty + 8 * s, 1);
@@ -144,6 +147,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             mbar_init(bar_tfull + 8 * a, 1);
             mbar_init(bar_tempty + 8 * a, 2 * EPI_WARPS);  // every epilogue warp of both CTAs
         }
+        for (int i = 0; i < 2 * EPI_WARPS; ++i) mbar_init(bar_res + 8 * i, 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_pair(smem_u32(tmem_holder), TMEM_COLS);
@@ -265,7 +269,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0;
         const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
         const bool has_res = (p.flags & DMPQ_EP_RESIDUAL) != 0;
-        const bool has_tdc = (p.flags & DMPQ_EP_TDC_REFRESH) != 0;
+        // gated residual with a bf16 output: the residual chunk arrives by TMA into the chunk's
+        // output staging buffer (coalesced; the lane-per-row global loads cost 30-50 us per GEMM)
+        const bool tma_res = has_res && p.Y != nullptr;
+        // the fused-refresh code only exists in the TDC instantiation (it costs the plain epilogue
+        // ~10 registers and spills in the INT8 kernel)
+        const bool has_tdc = TDC && (p.flags & DMPQ_EP_TDC_REFRESH) != 0;
         // fused TDC refresh statistics of this warp's rows / chunks over all its tiles (fixed order)
         double tacc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
@@ -289,11 +298,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             const int rowbase = mt * 256 + (int)rank * BM + q * 32;
             const int row = rowbase + lane;
             const bool row_ok = row < p.m;
-            if ((has_res || has_tdc) && row_ok && chalf == 0) {
+            if (((has_res && !tma_res) || has_tdc) && row_ok && chalf == 0) {
                 // this tile's row segments of the epilogue's global inputs -> L2 while the
                 // mainloop still runs (one bulk prefetch per row and tensor)
                 const uint32_t seg = (uint32_t)min(BN, p.n - n0) * 2;
-                if (has_res) bulk_prefetch_l2(p.residual + (size_t)row * p.ldr + n0, seg);
+                if (has_res && !tma_res) bulk_prefetch_l2(p.residual + (size_t)row * p.ldr + n0, seg);
                 if (has_tdc) {
                     bulk_prefetch_l2(p.tdc_x_in + (size_t)row * p.n + n0, seg);
                     bulk_prefetch_l2(p.tdc_delta + (size_t)row * p.n + n0, seg);
@@ -302,20 +311,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             float sa = 0.0f;
             if constexpr (I8) sa = row_ok ? p.a_scale[row] : 0.0f;
             const f2 sa2 = f2make(sa, sa);
-            mbar_wait(bar_tfull + 8 * acc, acc_phase);
-            tc_fence_after();
             const int n_here = min(BN, p.n - n0);
             const int nch_here = (n_here + 31) >> 5;
             const int my_last = nch_here > chalf ? chalf + ((nch_here - 1 - chalf) / CSTEP) * CSTEP : -1;
+            const int nmine = my_last < 0 ? 0 : (my_last - chalf) / CSTEP + 1;   // this warp's chunks of the tile
+            constexpr int NSB = L::STAGING_BUFS;
+            // residual chunk j of this warp -> staging buffer (chunk_ctr + j) % NSB, by TMA; the first
+            // NSB chunks are requested now, while the mainloop of this tile still runs
+            const uint32_t ctr0 = chunk_ctr;   // this tile's first chunk counter
+            auto res_load = [&](int j) {
+                const uint32_t cj = ctr0 + (uint32_t)j;
+                mbar_arrive_expect_tx(bar_res + 8 * (ew * 2 + (int)(cj % NSB)), 2048);
+                tma_load_2d(staging + (cj % NSB) * 2048, &tmR, n0 + (chalf + j * CSTEP) * 32, rowbase,
+                            bar_res + 8 * (ew * 2 + (int)(cj % NSB)));
+            };
+            if (tma_res && nmine > 0) {
+                if (lane == 0) {
+                    bulk_wait_read0();   // every earlier store of this warp has read its staging buffer
+                    for (int j = 0; j < NSB && j < nmine; ++j) res_load(j);
+                }
+                __syncwarp();
+            }
+            mbar_wait(bar_tfull + 8 * acc, acc_phase);
+            tc_fence_after();
             if (my_last < 0) {   // no chunk for this warp in a narrow tile: release TMEM right away
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
             }
             for (int c = chalf; c < nch_here; c += CSTEP) {
-                // gated-residual row chunk: loaded before the TMEM read so the two latencies overlap
+                const int jc = (c - chalf) / CSTEP;   // this warp's chunk index in the tile
+                const uint32_t buf = staging + (chunk_ctr % NSB) * 2048;
+                const uint32_t rbar = bar_res + 8 * (ew * 2 + (int)(chunk_ctr % NSB));
+                const uint32_t rphase = (chunk_ctr / NSB) & 1;
+                // gated-residual chunk (TMA-staged: requested ahead, see res_load; else loaded
+                // here, before the TMEM read so the two latencies overlap)
                 uint4 rv4[4];
-                if (has_res && row_ok) {
+                if (!tma_res && has_res && row_ok) {
                     const uint4* rp = reinterpret_cast<const uint4*>(p.residual + (size_t)row * p.ldr + n0 + c * 32);
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) rv4[v4] = __ldg(rp + v4);
@@ -366,6 +398,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                         y[j] = fma2(h, t, h);
                     }
                 }
+                if (tma_res) {   // this lane's row of the staged chunk (64-byte swizzle, as the store)
+                    mbar_wait(rbar, rphase);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4) {
+                        const uint32_t a = buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(rv4[v4].x), "=r"(rv4[v4].y), "=r"(rv4[v4].z), "=r"(rv4[v4].w) : "r"(a) : "memory");
+                    }
+                }
                 if (has_res && row_ok) {
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
@@ -386,12 +427,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
 #pragma unroll
                 for (int j = 0; j < 16; ++j) yb[j] = pack_bf16x2_f2(y[j]);
                 if (p.Y) {
-                    const uint32_t buf = staging + (L::STAGING_BUFS == 2 ? (chunk_ctr & 1) * 2048 : 0);
-                    if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
-                        if constexpr (L::STAGING_BUFS == 2) bulk_wait_read1();
-                        else bulk_wait_read0();
+                    if (!tma_res) {
+                        if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
+                            if constexpr (L::STAGING_BUFS == 2) bulk_wait_read1();
+                            else bulk_wait_read0();
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
                         const uint32_t a = buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);  // 64B swizzle
@@ -404,6 +446,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     if (lane == 0) {
                         tma_store_2d(&tmY, buf, col0, rowbase);
                         bulk_commit();
+                        if (tma_res && jc + NSB < nmine) {   // this buffer's next residual chunk, once the store has read it
+                            bulk_wait_read0();
+                            res_load(jc + NSB);
+                        }
                     }
                     ++chunk_ctr;
                 }
@@ -542,23 +588,24 @@ static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, i
     return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BN, int STAGES>
+template <int KIND, int BN, int STAGES, bool TDC = false>
 static dmpq_status set_pair_attrs() {
     using L = PairLayout<KIND, BN, STAGES>;
-    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              L::TOTAL) != cudaSuccess)
         return check_launch("dmpq_gemm(smem attribute)");
     return DMPQ_OK;
 }
 
-template <int KIND, int BN, int STAGES>
+template <int KIND, int BN, int STAGES, bool TDC = false>
 static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
     using L = PairLayout<KIND, BN, STAGES>;
     constexpr bool FP4 = KIND == 1;
-    CUtensorMap tmA, tmB, tmSFA, tmSFB, tmY;
+    CUtensorMap tmA, tmB, tmSFA, tmSFB, tmY, tmR;
     std::memset(&tmSFA, 0, sizeof(tmSFA));
     std::memset(&tmSFB, 0, sizeof(tmSFB));
     std::memset(&tmY, 0, sizeof(tmY));
+    std::memset(&tmR, 0, sizeof(tmR));
     if (!make_tmap(&tmA, a_codes, p.m, p.kbytes, BM) || !make_tmap(&tmB, w_codes, p.n, p.kbytes, BN / 2))
         return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (A/B)");
     if constexpr (FP4) {
@@ -568,20 +615,22 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     }
     if (p.Y && !make_tmap_y(&tmY, p.Y, p.m, p.n, p.ldy))
         return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (Y)");
+    if (p.Y && (p.flags & DMPQ_EP_RESIDUAL) && !make_tmap_y(&tmR, p.residual, p.m, p.n, p.ldr))
+        return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (residual)");
     p.num_m_tiles = (p.m + 255) / 256;
     p.num_n_tiles = (p.n + BN - 1) / BN;
     p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
-    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES>;
+    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC>;
     static bool attr_set = false;   // per process and kernel (dmpq_prepare sets them ahead of graph capture)
     if (!attr_set) {
-        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES>();
+        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES, TDC>();
         if (rc != DMPQ_OK) return rc;
         attr_set = true;
     }
     const int tiles = p.num_m_tiles * p.num_n_tiles;
     int clusters = num_sms() / 2;
     if (clusters > tiles) clusters = tiles;
-    kern<<<2 * clusters, 128 + 32 * EPI_WARPS, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, p);
+    kern<<<2 * clusters, 128 + 32 * EPI_WARPS, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, tmR, p);
     return check_launch("dmpq_gemm");
 }
 
@@ -624,6 +673,9 @@ extern "C" dmpq_status dmpq_prepare(void) {
         if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
     }
     if (rc == DMPQ_OK && fp4_bn() == 256) rc = set_pair_attrs<1, 256, 5>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<0, 256, 5, true>();   // fused TDC refresh variants
+    if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5, true>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5, true>();
     if (rc == DMPQ_OK) rc = prepare_quant_tma();
     if (rc == DMPQ_OK) rc = prepare_quant_had();
     return rc;
@@ -673,6 +725,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
     }
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_gemm: needs an sm_100 device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+    const bool tdc = (p.flags & DMPQ_EP_TDC_REFRESH) != 0;
     if (fp4) {
         DMPQ_REQUIRE(A->codes && A->sf && A->g && W->fp4_codes && W->fp4_sf && W->fp4_g && aligned16(A->codes) &&
                          aligned16(A->sf) && aligned16(W->fp4_codes) && aligned16(W->fp4_sf),
@@ -681,6 +734,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
+        if (tdc) return launch_gemm_pair<1, 192, 5, true>(p, A->codes, W->fp4_codes, st);
         if (fp4_bn() == 256) return launch_gemm_pair<1, 256, 5>(p, A->codes, W->fp4_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st)
                                  : launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
@@ -688,6 +742,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         DMPQ_REQUIRE(A->codes && W->bf16_w && aligned16(A->codes) && aligned16(W->bf16_w), DMPQ_EALIGN,
                      "dmpq_gemm: BF16 path needs A->codes (bf16 activation) and W->bf16_w");
         p.kbytes = 2 * k;
+        if (tdc) return launch_gemm_pair<2, 256, 5, true>(p, A->codes, W->bf16_w, st);
         return gemm_stages() == 5 ? launch_gemm_pair<2, 256, 5>(p, A->codes, W->bf16_w, st)
                                  : launch_gemm_pair<2, 256, 6>(p, A->codes, W->bf16_w, st);
     } else {
@@ -695,6 +750,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
                      DMPQ_EALIGN, "dmpq_gemm: INT8 operand pointers");
         p.kbytes = k;
         p.a_scale = A->row_scale; p.w_scale = W->i8_scale;
+        if (tdc) return launch_gemm_pair<0, 256, 5, true>(p, A->codes, W->i8_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st)
                                  : launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);
     }

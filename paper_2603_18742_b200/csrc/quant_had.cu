@@ -153,7 +153,6 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
     const uint32_t tx_bytes = (uint32_t)(R * nb * 256);
     const Seg8 sr{red, grp * (tpr >> 3), tpr >> 3};
     const bool want_fp4 = p.fp4_codes != nullptr, want_i8 = p.i8_codes != nullptr;
-    constexpr bool pdr = PDR;   // p.row_abs_sum or p.amax_in requested
 
     // NVFP4 block-scale constants: raw = fl(fl(a/6)/g) takes the exact fast division when g is
     // in [2^-90, 2^90] and the block maxima in [a_lo, a_hi] (fastmath.cuh), else __fdiv_rn.
