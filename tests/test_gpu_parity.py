@@ -289,7 +289,8 @@ def test_tdc_nvfp4_cache(D, orc, m, h):
     assert np.array_equal(synth.bits(x.cpu()), ref)
 
 
-@pytest.mark.parametrize("m,k,ln", [(5, 128, False), (130, 3072, True), (37, 1920, False), (33, 12288, False)])
+@pytest.mark.parametrize("m,k,ln", [(5, 128, False), (130, 3072, True), (37, 1920, False), (33, 12288, False),
+                                    (19, 7680, True), (41, 640, True), (23, 9216, False), (3, 16384, True)])
 def test_quantize_hadamard_bit_exact(D, orc, m, k, ln):
     """Online block Hadamard fused into the quantizer (R14): codes and scales
     equal the oracle's FP32 FHT followed by the FP32-input quantizers."""
@@ -312,8 +313,9 @@ def test_quantize_hadamard_bit_exact(D, orc, m, k, ln):
     assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
 
 
-@pytest.mark.parametrize("k,ln", [(3072, False), (3072, True), (12288, False)])
-def test_quantize_hadamard_dense_rows(D, orc, k, ln):
+@pytest.mark.parametrize("k,ln,which", [(3072, False, "both"), (3072, True, "both"), (12288, False, "both"),
+                                        (3072, True, "nvfp4"), (3072, True, "int8"), (12288, False, "int8")])
+def test_quantize_hadamard_dense_rows(D, orc, k, ln, which):
     """Several thousand full rows through the Hadamard quantizer (both formats): enough
     elements that fl(y r) lands exactly on INT8 / E2M1 rounding ties many times, so a
     contracted multiply-add (one rounding instead of RNE(fl(y r))) cannot pass."""
@@ -324,17 +326,20 @@ def test_quantize_hadamard_dense_rows(D, orc, k, ln):
     a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
     a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
     amax = torch.zeros(1, device="cuda")
-    D.dmpq_quantize_act(x.cuda(), out_i8=a8, out_fp4=a4, amax_out=amax, layernorm=ln, h_out=h, hadamard=True)
+    D.dmpq_quantize_act(x.cuda(), out_i8=a8 if which != "nvfp4" else None, out_fp4=a4 if which != "int8" else None,
+                        amax_out=amax, layernorm=ln, h_out=h, hadamard=True)
     torch.cuda.synchronize()
     src = synth.bits(h.cpu()) if ln else synth.bits(x)
     y = orc.fht128(orc.bf16_to_f32(src).reshape(m, k))
     assert amax.item() == float(np.abs(y).max())
-    c8, s8 = orc.int8_quantize_f32(y)
-    assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
-    assert np.array_equal(a8.codes.cpu().numpy(), c8)
-    c4, s4 = orc.nvfp4_quantize_f32(y, 0.004)
-    assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s4)
-    assert np.array_equal(a4.codes.cpu().numpy(), c4)
+    if which != "nvfp4":
+        c8, s8 = orc.int8_quantize_f32(y)
+        assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+        assert np.array_equal(a8.codes.cpu().numpy(), c8)
+    if which != "int8":
+        c4, s4 = orc.nvfp4_quantize_f32(y, 0.004)
+        assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s4)
+        assert np.array_equal(a4.codes.cpu().numpy(), c4)
 
 
 @pytest.mark.parametrize("k", [128, 1920])
