@@ -134,7 +134,8 @@ __device__ __forceinline__ uint32_t int8x4_magic(f2 y01, f2 y23, f2 r2, f2 z2) {
 #ifndef DMPQ_HAD_LN_MINB
 #define DMPQ_HAD_LN_MINB 3   // CTAs per SM the LN variant is register-limited for (experiments)
 #endif
-template <bool LN, bool PDR, bool WH>   // WH: write h (LN variants only)
+// WH: write h (LN variants only). FMT: 1 NVFP4 only, 2 INT8 only, 3 both, 0 from the pointers.
+template <bool LN, bool PDR, bool WH, int FMT = 0>
 __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_kernel(const QuantParams p, const __grid_constant__ CUtensorMap tmX,
                                                               int tpr, int R, int set_stride, int nbuf, int split) {
     extern __shared__ uint8_t hsm_raw[];
@@ -152,7 +153,8 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
     const int iters = (int)blockIdx.x < nsets ? (nsets - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const uint32_t tx_bytes = (uint32_t)(R * nb * 256);
     const Seg8 sr{red, grp * (tpr >> 3), tpr >> 3};
-    const bool want_fp4 = p.fp4_codes != nullptr, want_i8 = p.i8_codes != nullptr;
+    const bool want_fp4 = FMT ? (FMT & 1) != 0 : p.fp4_codes != nullptr;
+    const bool want_i8 = FMT ? (FMT & 2) != 0 : p.i8_codes != nullptr;
 
     // NVFP4 block-scale constants: raw = fl(fl(a/6)/g) takes the exact fast division when g is
     // in [2^-90, 2^90] and the block maxima in [a_lo, a_hi] (fastmath.cuh), else __fdiv_rn.
@@ -449,9 +451,12 @@ int had_ctas_per_sm(int threads, int smem) {
 }  // namespace
 
 dmpq_status prepare_quant_had() {
-    const void* kernels[] = {(const void*)quant_had_kernel<false, false, false>, (const void*)quant_had_kernel<true, false, false>,
-                             (const void*)quant_had_kernel<true, false, true>,   (const void*)quant_had_kernel<false, true, false>,
-                             (const void*)quant_had_kernel<true, true, false>,   (const void*)quant_had_kernel<true, true, true>};
+    const void* kernels[] = {(const void*)quant_had_kernel<false, false, false, 1>, (const void*)quant_had_kernel<false, false, false, 2>,
+                             (const void*)quant_had_kernel<false, false, false, 3>, (const void*)quant_had_kernel<true, false, false, 1>,
+                             (const void*)quant_had_kernel<true, false, false, 2>,  (const void*)quant_had_kernel<true, false, false, 3>,
+                             (const void*)quant_had_kernel<true, false, true>,      (const void*)quant_had_kernel<false, true, false>,
+                             (const void*)quant_had_kernel<true, true, false>,      (const void*)quant_had_kernel<true, true, true>,
+                             (const void*)quant_had_kernel<false, false, false>,    (const void*)quant_had_kernel<true, false, false>};
     bool ok = true;
     for (const void* k : kernels)
         ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) == cudaSuccess;
@@ -492,9 +497,15 @@ dmpq_status launch_quant_had(const QuantParams& p, cudaStream_t s) {
     const bool wh = ln && (p.flags & DMPQ_QF_WRITE_H) != 0;
 #define DMPQ_HAD_LAUNCH(a, b, c) quant_had_kernel<a, b, c><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split)
     if (ln && pdr) { if (wh) DMPQ_HAD_LAUNCH(true, true, true); else DMPQ_HAD_LAUNCH(true, true, false); }
-    else if (ln) { if (wh) DMPQ_HAD_LAUNCH(true, false, true); else DMPQ_HAD_LAUNCH(true, false, false); }
     else if (pdr) DMPQ_HAD_LAUNCH(false, true, false);
-    else DMPQ_HAD_LAUNCH(false, false, false);
+    else if (ln && wh) DMPQ_HAD_LAUNCH(true, false, true);
+    else {   // the common cases: formats fixed at compile time
+        const int fmt = (p.fp4_codes ? 1 : 0) | (p.i8_codes ? 2 : 0);
+#define DMPQ_HAD_LAUNCH_F(a, f) quant_had_kernel<a, false, false, f><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split)
+        if (ln) { if (fmt == 1) DMPQ_HAD_LAUNCH_F(true, 1); else if (fmt == 2) DMPQ_HAD_LAUNCH_F(true, 2); else if (fmt == 3) DMPQ_HAD_LAUNCH_F(true, 3); else DMPQ_HAD_LAUNCH(true, false, false); }
+        else { if (fmt == 1) DMPQ_HAD_LAUNCH_F(false, 1); else if (fmt == 2) DMPQ_HAD_LAUNCH_F(false, 2); else if (fmt == 3) DMPQ_HAD_LAUNCH_F(false, 3); else DMPQ_HAD_LAUNCH(false, false, false); }
+#undef DMPQ_HAD_LAUNCH_F
+    }
 #undef DMPQ_HAD_LAUNCH
     return check_launch("dmpq_quantize_act");
 }
