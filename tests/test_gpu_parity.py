@@ -152,6 +152,38 @@ def test_gemm_int8_bit_exact(D, orc, m, n, k):
     assert torch.equal(y.cpu(), torch.from_numpy(y_ref).to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("fmt,m,n,k", [(0, 300, 512, 256), (1, 300, 512, 256), (0, 1029, 1920, 512),
+                                       (1, 1029, 1920, 512), (0, 4133, 3072, 128), (1, 4133, 3072, 128)])
+def test_gemm_gated_residual(D, orc, fmt, m, n, k):
+    """Gated-residual epilogue y = fma(gate, y, residual): the TMA-staged residual (bf16 output
+    path, chunks requested a tile ahead, many tiles per CTA) equals the lane-per-row residual
+    path (FP32-only output) bit for bit, and the bf16 output is the RNE of the FP32 one; INT8
+    against the oracle's exact epilogue within the last FP32 rounding of the fma."""
+    x = synth.dit_activation(m, k, seed=m + 2 * k)
+    w, b = synth.linear_weight(n, k, seed=n + 3 * k)
+    pw = D.dmpq_pack_weights(w.cuda(), b)
+    g = torch.tensor([0.01], device="cuda")
+    a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == 1 else None)
+    D.dmpq_quantize_act(x.cuda(), out_fp4=a if fmt == 1 else None, out_i8=a if fmt == 0 else None)
+    res = synth.dit_activation(m, n, seed=m + 7, outlier_frac=0, tail_frac=0).cuda()
+    gate = (0.05 * torch.rand(n, generator=torch.Generator().manual_seed(n))).cuda()
+    y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    y32_tma = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    y32_lane = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y, Y32=y32_tma, residual=res, gate=gate)
+    D.dmpq_gemm(a, pw, Y32=y32_lane, residual=res, gate=gate)
+    torch.cuda.synchronize()
+    assert torch.equal(y32_tma.cpu(), y32_lane.cpu())
+    assert torch.equal(y.cpu(), y32_tma.cpu().to(torch.bfloat16))
+    if fmt == 0:
+        _, y_lin = orc.gemm_int8(a.codes.cpu().numpy(), a.row_scale.cpu().numpy(), pw.i8_codes.cpu().numpy(),
+                                 pw.i8_scale.cpu().numpy(), b.numpy())
+        ref = (gate.cpu().numpy().astype(np.float64)[None, :] * y_lin.astype(np.float64)
+               + res.cpu().float().numpy().astype(np.float64))
+        got = y32_tma.cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(got - ref) <= np.abs(ref) * 2.0 ** -23 + 1e-30)
+
+
 @pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
 def test_gemm_nvfp4_rel_l2(D, orc, m, n, k):
     x = synth.dit_activation(m, k, seed=5 * m + k)
