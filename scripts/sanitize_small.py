@@ -38,5 +38,23 @@ am = torch.zeros(1, device=dev)
 D.tdc_delta_amax(xi, xo, am)
 D.tdc_step_nvfp4(1, xi, xo, cache, g_new=torch.tensor([0.01], device=dev), amax_out=am, stats_out=st, workspace=ws)
 D.tdc_step_nvfp4(0, xi, xo, cache)
+# gated-residual epilogue (TMA-staged residual, chunks requested a tile ahead: several tiles per
+# CTA at this size) and the fused TDC refresh epilogue, both formats
+m2, n2, k2 = 1200, 3072, 128
+x2 = synth.dit_activation(m2, k2, seed=5).to(dev)
+w2, b2 = synth.linear_weight(n2, k2, seed=6)
+pw2 = D.dmpq_pack_weights(w2.to(dev), b2.to(dev))
+res = synth.dit_activation(m2, n2, seed=7).to(dev)
+gate = torch.full((n2,), 0.01, device=dev)
+y2 = torch.empty(m2, n2, dtype=torch.bfloat16, device=dev)
+d2 = torch.zeros(m2, n2, dtype=torch.bfloat16, device=dev)
+xin2 = synth.dit_activation(m2, n2, seed=8).to(dev)
+wsg = torch.zeros(D.dmpq_gemm_tdc_workspace_bytes(), dtype=torch.uint8, device=dev)
+for fmt in (D.FMT_INT8, D.FMT_NVFP4):
+    a = D.QuantAct.empty(fmt, m2, k2, dev, g=torch.tensor([0.01], device=dev) if fmt == D.FMT_NVFP4 else None)
+    D.dmpq_quantize_act(x2, out_fp4=a if fmt == D.FMT_NVFP4 else None, out_i8=a if fmt == D.FMT_INT8 else None,
+                        hadamard=True)
+    D.dmpq_gemm(a, pw2, Y=y2, residual=res, gate=gate)
+    D.dmpq_gemm(a, pw2, Y=y2, residual=res, gate=gate, tdc_x_in=xin2, tdc_delta=d2, tdc_stats=st, tdc_workspace=wsg)
 torch.cuda.synchronize()
 print("sanitize_small ok")
