@@ -395,13 +395,25 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
             *reinterpret_cast<uint32_t*>(sf_row_ptr(p.fp4_sf, p.kc4, r) + (size_t)c4 * 512) = 0u;
         }
     }
-    if (p.amax_out) {
-        const float am = warp_max(my_amax);
-        if (lane == 0) atomic_max_nonneg(p.amax_out, am);
-    }
-    if (p.amax_in) {
-        const float am = warp_max(my_amax_in);
-        if (lane == 0) atomic_max_nonneg(p.amax_in, am);
+    // tensor maxima: warp -> CTA in shared memory, one atomic per CTA (order-independent)
+    if (p.amax_out || p.amax_in) {
+        const float am = warp_max(my_amax), ai = warp_max(my_amax_in);
+        const int nw = (int)(blockDim.x + 31) >> 5;
+        __syncthreads();   // every row reduction of the loop has read its slots
+        if (lane == 0) {
+            hsts_f32(red + 4u * (tid >> 5), am);
+            hsts_f32(red + 4u * (H_MAX_SEG + (tid >> 5)), ai);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            float m0 = 0.0f, m1 = 0.0f;
+            for (int w = 0; w < nw; ++w) {
+                m0 = fmaxf(m0, hlds_f32(red + 4u * w));
+                m1 = fmaxf(m1, hlds_f32(red + 4u * (H_MAX_SEG + w)));
+            }
+            if (p.amax_out) atomic_max_nonneg(p.amax_out, m0);
+            if (p.amax_in) atomic_max_nonneg(p.amax_in, m1);
+        }
     }
 }
 
