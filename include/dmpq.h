@@ -94,6 +94,10 @@ typedef struct {
     float* i8_scale;       /* [n]: per-output-channel scale */
     const float* bias;     /* [n] or NULL (may point at caller memory) */
     const uint16_t* bf16_w;/* [n x k] original bf16 weights for the BF16 fallback (R15), or NULL */
+    const float* fp4_g_col;/* [n] per-output-column g_w, or NULL (fp4_g for every column): several
+                              layers packed side by side along n (e.g. Q, K, V over the same input)
+                              keep their own per-tensor scales; the NVFP4 epilogue then uses
+                              fl(g_a * fp4_g_col[n]) per column, bit-identical to separate GEMMs */
 } dmpq_weights;
 
 /* A quantized activation tensor, as written by dmpq_quantize_act. */

@@ -30,7 +30,8 @@ STATS_LEN = 7
 
 class Weights(ctypes.Structure):
     _fields_ = [("n", c_int), ("k", c_int), ("fp4_codes", c_void_p), ("fp4_sf", c_void_p), ("fp4_g", c_void_p),
-                ("i8_codes", c_void_p), ("i8_scale", c_void_p), ("bias", c_void_p), ("bf16_w", c_void_p)]
+                ("i8_codes", c_void_p), ("i8_scale", c_void_p), ("bias", c_void_p), ("bf16_w", c_void_p),
+                ("fp4_g_col", c_void_p)]
 
 
 class Act(ctypes.Structure):

@@ -49,9 +49,10 @@ def default_tau_gamma(tau_rel: float = 0.0025, beta: float = 0.001):
 
 @dataclass
 class BlockWeights:
-    layers: list            # 6 PackedWeights
+    layers: list            # 6 PackedWeights (Q, K, V are views into qkv)
     g1: torch.Tensor        # [H] fp32 gate of the attention residual
     g2: torch.Tensor        # [H] fp32 gate of the FFN residual
+    qkv: D.PackedWeights = None   # Q, K, V side by side (one GEMM when they share a format)
 
     def nbytes(self):
         return sum(w.nbytes() for w in self.layers)
@@ -69,11 +70,12 @@ def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, had
         layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard, keep_bf16=keep_bf16))
         if not keep_bf16:
             del w
+    qkv, layers[0:3] = D.dmpq_concat_weights(layers[0:3])
     g = torch.Generator(device="cpu")
     g.manual_seed(seed * 16 + 15)
     g1 = (gate_scale * (0.5 + torch.rand(H, generator=g))).to(device)
     g2 = (gate_scale * (0.5 + torch.rand(H, generator=g))).to(device)
-    return BlockWeights(layers, g1, g2)
+    return BlockWeights(layers, g1, g2, qkv)
 
 
 class Workspace:
@@ -82,8 +84,9 @@ class Workspace:
     def __init__(self, m: int, H: int, F: int, device, g_table: torch.Tensor):
         self.m, self.H, self.F = m, H, F
         e = dict(dtype=torch.bfloat16, device=device)
-        self.qk = torch.empty(m, H, **e)         # Q and K outputs (unused by the stand-in attention)
-        self.v = torch.empty(m, H, **e)
+        self.qkv = torch.empty(m, 3 * H, **e)    # Q | K | V outputs (Q, K unused by the stand-in attention)
+        self.qk = self.qkv[:, :H]
+        self.v = self.qkv[:, 2 * H:]
         self.x_mid = torch.empty(m, H, **e)
         self.f = torch.empty(m, F, **e)
         self.g_table = g_table                     # [n_blocks, 4] fp32 NVFP4 global scales
@@ -122,7 +125,7 @@ class DiTStack:
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
                  tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False,
-                 fuse_refresh: bool = False):
+                 fuse_refresh: bool = False, fuse_qkv: bool = True):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -137,6 +140,7 @@ class DiTStack:
         # bf16 cache, optional: the TDC refresh runs in the FFN2 GEMM's epilogue (
         # measured slower than the streaming refresh kernel)
         self.fuse_refresh = fuse_refresh and not cache_nvfp4
+        self.fuse_qkv = fuse_qkv      # one Q|K|V GEMM when the three layers share a format
         self.m_total = m_total if m_total is not None else m_local
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
@@ -242,9 +246,15 @@ class DiTStack:
         if cap:
             self._cap("x_in", x_in); self._cap("h1", ws.h1)
             self._cap_act("a0_i8", q0[D.FMT_INT8]); self._cap_act("a0_f4", q0[D.FMT_NVFP4])
-        for j, out in ((0, ws.qk), (1, ws.qk), (2, ws.v)):
-            self._gemm(q0[fmts[j]], W.layers[j], Y=out)
-            self._cap(f"y{j}", out)
+        if self.fuse_qkv and fmts[0] == fmts[1] == fmts[2]:
+            # one GEMM over the side-by-side Q | K | V weights (per-layer NVFP4 g_w per column)
+            self._gemm(q0[fmts[0]], W.qkv, Y=ws.qkv)
+            for j in range(3):
+                self._cap(f"y{j}", ws.qkv[:, j * H:(j + 1) * H])
+        else:
+            for j, out in ((0, ws.qk), (1, ws.qkv[:, H:2 * H]), (2, ws.v)):
+                self._gemm(q0[fmts[j]], W.layers[j], Y=out)
+                self._cap(f"y{j}", out)
         # O projection on the attention stand-in a = v, gated residual in the epilogue
         q1 = self._quant(b, 1, ws.v, {fmts[3]})
         if fmts[3] != D.FMT_BF16:
@@ -380,7 +390,11 @@ class DiTStack:
                 flops = 0.0 if d == L.TDC_DECIDE_SKIP else 2.0 * self.m * (4 * self.H * self.H + 2 * self.H * self.F)
             else:
                 flops = self._block_work(b, x_in, x_out, d, fmts, first)
-            self.launches += 1 if d == L.TDC_DECIDE_SKIP else (13 if first else (10 if self.fuse_refresh else 11))
+            if d == L.TDC_DECIDE_SKIP:
+                self.launches += 1
+            else:   # 4 quantizers + 6 GEMMs + refresh, fewer when fused, +2 for a cache bootstrap
+                qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2]
+                self.launches += 11 - (1 if self.fuse_refresh else 0) - (2 if qkv1 else 0) + (2 if first else 0)
             rec.linear_flops += flops
             rec.fmts.append(None if d == L.TDC_DECIDE_SKIP else fmts)
             rec.gammas.append(gamma)

@@ -41,6 +41,7 @@ struct GemmParams {
     const uint8_t* sfb;
     const float* g_a;
     const float* g_w;
+    const float* g_w_col;  // [n] per-column g_w (layers packed side by side) or NULL
     int kc4;               // scale atoms per 128-row tile (= k/64)
     int sfb_row_tiles;     // ceil(n/128)
     // epilogue
@@ -260,8 +261,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         const int etid = threadIdx.x - 128;
         int local = 0;
         uint32_t chunk_ctr = 0;
-        float gg = 0.0f;
-        if constexpr (FP4) gg = __fmul_rn(*p.g_a, *p.g_w);
+        float gg = 0.0f, ga = 0.0f;
+        const bool gcol = FP4 && p.g_w_col != nullptr;
+        if constexpr (FP4) {
+            ga = *p.g_a;
+            if (!gcol) gg = __fmul_rn(ga, *p.g_w);
+        }
         else if constexpr (!I8) gg = 1.0f;   // BF16: y = fma(acc, 1, bias) = fl(acc + bias)
         const f2 gg2 = f2make(gg, gg);
         const uint32_t staging = sbase + L::STAGING_OFFSET + ew * (L::STAGING_BUFS * 2048);
@@ -288,7 +293,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                 const int col = n0 + i;
                 const bool ok = col < p.n;
                 const float bv = (ok && has_bias) ? p.bias[col] : -0.0f;   // fma(x, s, -0) == fl(x * s) exactly
-                const float wv = (I8 && ok) ? p.w_scale[col] : 0.0f;
+                // INT8: s_w[n]; NVFP4 with per-column g_w: fl(g_a g_w[n]) (same product as gg)
+                const float wv = (I8 && ok) ? p.w_scale[col] : ((FP4 && ok && gcol) ? __fmul_rn(ga, p.g_w_col[col]) : 0.0f);
                 const float gv = (ok && has_res) ? p.gate[col] : 0.0f;
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + i * 4), "f"(bv) : "memory");
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(vb + (BN + i) * 4), "f"(wv) : "memory");
@@ -371,9 +377,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     if constexpr (!I8) {
                         const f2 a0 = f2make(__uint_as_float(r[4 * v4]), __uint_as_float(r[4 * v4 + 1]));
                         const f2 a1 = f2make(__uint_as_float(r[4 * v4 + 2]), __uint_as_float(r[4 * v4 + 3]));
+                        f2 g0 = gg2, g1 = gg2;
+                        if (gcol) {   // per-column fl(g_a g_w[n]) staged with the tile's vectors
+                            float w0, w1, w2, w3;
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(w0), "=f"(w1), "=f"(w2), "=f"(w3) : "r"(vb + (BN + c * 32 + v4 * 4) * 4));
+                            g0 = f2make(w0, w1);
+                            g1 = f2make(w2, w3);
+                        }
                         // y = fma(acc, g_a*g_w, bias): one rounding (FP32 tolerance path, R3)
-                        y[2 * v4] = fma2(a0, gg2, bb0);
-                        y[2 * v4 + 1] = fma2(a1, gg2, bb1);
+                        y[2 * v4] = fma2(a0, g0, bb0);
+                        y[2 * v4 + 1] = fma2(a1, g1, bb1);
                     } else {
                         float w0, w1, w2, w3;
                         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -731,7 +745,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
                          aligned16(A->sf) && aligned16(W->fp4_codes) && aligned16(W->fp4_sf),
                      DMPQ_EALIGN, "dmpq_gemm: NVFP4 operand pointers");
         p.kbytes = k / 2;
-        p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g;
+        p.sfa = A->sf; p.sfb = W->fp4_sf; p.g_a = A->g; p.g_w = W->fp4_g; p.g_w_col = W->fp4_g_col;
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
         if (tdc) return launch_gemm_pair<1, 192, 5, true>(p, A->codes, W->fp4_codes, st);

@@ -86,6 +86,46 @@ class PackedWeights:
         return sum(t.numel() * t.element_size() for t in
                    (self.fp4_codes, self.fp4_sf, self.fp4_g, self.i8_codes, self.i8_scale))
 
+    @classmethod
+    def _from_tensors(cls, n, k, codes, sf, g, i8, i8s, bias, bf16_w, hadamard, g_col=None):
+        pw = cls(n, k, codes, sf, g, i8, i8s, bias, hadamard=hadamard, bf16_w=bf16_w)
+        pw.g_col = g_col
+        pw.c = L.Weights(n, k, codes.data_ptr(), sf.data_ptr(), g.data_ptr(), i8.data_ptr(), i8s.data_ptr(),
+                         None if bias is None else bias.data_ptr(), None if bf16_w is None else bf16_w.data_ptr(),
+                         None if g_col is None else g_col.data_ptr())
+        return pw
+
+
+def dmpq_concat_weights(pws: list) -> tuple:
+    """Pack several layers over the same input side by side along n (e.g. Q, K, V): returns the
+    concatenated PackedWeights (each layer keeps its own NVFP4 g_w through fp4_g_col, so one GEMM
+    gives the separate GEMMs' outputs bit for bit) and per-layer views into it (same contents as
+    the inputs, which can then be freed). Needs every n % 128 == 0 (whole scale-atom row tiles)."""
+    k = pws[0].k
+    if any(p.k != k or p.n % 128 for p in pws) or len({p.hadamard for p in pws}) != 1:
+        raise ValueError("dmpq_concat_weights: equal k, n % 128 == 0 and one Hadamard setting required")
+    has_bias = all(p.bias is not None for p in pws)
+    has_bf16 = all(p.bf16_w is not None for p in pws)
+    n = sum(p.n for p in pws)
+    codes = torch.cat([p.fp4_codes for p in pws])
+    sf = torch.cat([p.fp4_sf for p in pws])
+    i8 = torch.cat([p.i8_codes for p in pws])
+    i8s = torch.cat([p.i8_scale for p in pws])
+    bias = torch.cat([p.bias for p in pws]) if has_bias else None
+    bf16_w = torch.cat([p.bf16_w for p in pws]) if has_bf16 else None
+    g_col = torch.cat([p.fp4_g.expand(p.n) for p in pws]).contiguous()
+    cat = PackedWeights._from_tensors(n, k, codes, sf, g_col[:1], i8, i8s, bias, bf16_w, pws[0].hadamard, g_col)
+    views, r0, s0 = [], 0, 0
+    for p in pws:
+        ns = p.fp4_sf.numel()
+        views.append(PackedWeights._from_tensors(
+            p.n, k, codes[r0:r0 + p.n], sf[s0:s0 + ns], g_col[r0:r0 + 1], i8[r0:r0 + p.n], i8s[r0:r0 + p.n],
+            None if bias is None else bias[r0:r0 + p.n], None if bf16_w is None else bf16_w[r0:r0 + p.n],
+            p.hadamard))
+        r0 += p.n
+        s0 += ns
+    return cat, views
+
 
 def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamard: bool = False,
                       keep_bf16: bool = False) -> PackedWeights:

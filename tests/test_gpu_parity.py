@@ -184,6 +184,45 @@ def test_gemm_gated_residual(D, orc, fmt, m, n, k):
         assert np.all(np.abs(got - ref) <= np.abs(ref) * 2.0 ** -23 + 1e-30)
 
 
+@pytest.mark.parametrize("fmt,m,k,had", [(0, 300, 256, False), (1, 300, 256, False), (1, 1029, 512, True),
+                                        (0, 1029, 512, True), (2, 257, 128, False)])
+def test_gemm_concatenated_layers(D, orc, fmt, m, k, had):
+    """Q, K, V packed side by side (dmpq_concat_weights: per-column NVFP4 g_w): one GEMM gives
+    the three separate GEMMs' outputs bit for bit; the per-layer views pack what the inputs did."""
+    ns = (384, 256, 512)
+    packs, ws = [], []
+    for j, n in enumerate(ns):
+        w, b = synth.linear_weight(n, k, seed=40 + j)
+        ws.append(w)
+        packs.append(D.dmpq_pack_weights(w.cuda(), b, hadamard=had, keep_bf16=(fmt == 2)))
+    ref = [(p.fp4_codes.clone(), p.fp4_sf.clone(), p.fp4_g.clone(), p.i8_codes.clone(), p.i8_scale.clone())
+           for p in packs]
+    assert len({float(p.fp4_g.item()) for p in packs}) == 3   # distinct per-layer scales
+    cat, views = D.dmpq_concat_weights(packs)
+    for v, r in zip(views, ref):
+        for a_, b_ in zip((v.fp4_codes, v.fp4_sf, v.fp4_g, v.i8_codes, v.i8_scale), r):
+            assert torch.equal(a_, b_)
+    x = synth.dit_activation(m, k, seed=m + k)
+    g = torch.tensor([0.01], device="cuda")
+    if fmt == 2:
+        a = D.QuantAct.bf16(x.cuda())
+    else:
+        a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == 1 else None)
+        D.dmpq_quantize_act(x.cuda(), out_fp4=a if fmt == 1 else None, out_i8=a if fmt == 0 else None, hadamard=had)
+    y_cat = torch.empty(m, sum(ns), dtype=torch.bfloat16, device="cuda")
+    y32_cat = torch.empty(m, sum(ns), dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a, cat, Y=y_cat, Y32=y32_cat)
+    c0 = 0
+    for v, n in zip(views, ns):
+        y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+        y32 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+        D.dmpq_gemm(a, v, Y=y, Y32=y32)
+        torch.cuda.synchronize()
+        assert torch.equal(y32_cat[:, c0:c0 + n].cpu(), y32.cpu())
+        assert torch.equal(y_cat[:, c0:c0 + n].cpu(), y.cpu())
+        c0 += n
+
+
 @pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
 def test_gemm_nvfp4_rel_l2(D, orc, m, n, k):
     x = synth.dit_activation(m, k, seed=5 * m + k)
