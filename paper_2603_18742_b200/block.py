@@ -59,7 +59,7 @@ class BlockWeights:
 
 
 def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, hadamard: bool = False,
-                       keep_bf16: bool = False) -> BlockWeights:
+                       keep_bf16: bool = False, fuse_qkv: bool = True) -> BlockWeights:
     shapes = [(H, H), (H, H), (H, H), (H, H), (F, H), (H, F)]
     layers = []
     for j, (n, k) in enumerate(shapes):
@@ -70,7 +70,9 @@ def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, had
         layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard, keep_bf16=keep_bf16))
         if not keep_bf16:
             del w
-    qkv, layers[0:3] = D.dmpq_concat_weights(layers[0:3])
+    qkv = None
+    if fuse_qkv:   # needs H % 128 == 0 (whole scale-atom row tiles per layer)
+        qkv, layers[0:3] = D.dmpq_concat_weights(layers[0:3])
     g = torch.Generator(device="cpu")
     g.manual_seed(seed * 16 + 15)
     g1 = (gate_scale * (0.5 + torch.rand(H, generator=g))).to(device)
@@ -86,7 +88,8 @@ class Workspace:
         e = dict(dtype=torch.bfloat16, device=device)
         self.qkv = torch.empty(m, 3 * H, **e)    # Q | K | V outputs (Q, K unused by the stand-in attention)
         self.qk = self.qkv[:, :H]
-        self.v = self.qkv[:, 2 * H:]
+        self.v = self.qkv[:, 2 * H:]             # strided view (row stride 3H): quantizer input only
+        self.v_dense = torch.empty(m, H, **e)     # V when the O projection runs the BF16 GEMM (dense A, R15)
         self.x_mid = torch.empty(m, H, **e)
         self.f = torch.empty(m, F, **e)
         self.g_table = g_table                     # [n_blocks, 4] fp32 NVFP4 global scales
@@ -144,8 +147,8 @@ class DiTStack:
         self.m_total = m_total if m_total is not None else m_local
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
-        self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr)
-                       for b in range(n_blocks)]
+        self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr,
+                                          fuse_qkv=fuse_qkv) for b in range(n_blocks)]
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
         # one buffer for the per-step MAX all-reduce: [0] amax of the quantised values (NVFP4 global
         # scales, R3); [1] max|x| of the layer inputs (PDR, R15); then max|d| of each block's last
@@ -246,17 +249,20 @@ class DiTStack:
         if cap:
             self._cap("x_in", x_in); self._cap("h1", ws.h1)
             self._cap_act("a0_i8", q0[D.FMT_INT8]); self._cap_act("a0_f4", q0[D.FMT_NVFP4])
-        if self.fuse_qkv and fmts[0] == fmts[1] == fmts[2]:
+        # the BF16 GEMM reads its A operand densely (row stride k): a BF16-routed O projection
+        # gets V in its own buffer instead of the strided Q|K|V view
+        v = ws.v_dense if fmts[3] == D.FMT_BF16 else ws.v
+        if self.fuse_qkv and fmts[0] == fmts[1] == fmts[2] and v is ws.v:
             # one GEMM over the side-by-side Q | K | V weights (per-layer NVFP4 g_w per column)
             self._gemm(q0[fmts[0]], W.qkv, Y=ws.qkv)
             for j in range(3):
                 self._cap(f"y{j}", ws.qkv[:, j * H:(j + 1) * H])
         else:
-            for j, out in ((0, ws.qk), (1, ws.qkv[:, H:2 * H]), (2, ws.v)):
+            for j, out in ((0, ws.qk), (1, ws.qkv[:, H:2 * H]), (2, v)):
                 self._gemm(q0[fmts[j]], W.layers[j], Y=out)
                 self._cap(f"y{j}", out)
         # O projection on the attention stand-in a = v, gated residual in the epilogue
-        q1 = self._quant(b, 1, ws.v, {fmts[3]})
+        q1 = self._quant(b, 1, v, {fmts[3]})
         if fmts[3] != D.FMT_BF16:
             self._cap_act("a1", q1[fmts[3]])
         self._gemm(q1[fmts[3]], W.layers[3], Y=ws.x_mid, residual=x_in, gate=W.g1)
@@ -393,7 +399,7 @@ class DiTStack:
             if d == L.TDC_DECIDE_SKIP:
                 self.launches += 1
             else:   # 4 quantizers + 6 GEMMs + refresh, fewer when fused, +2 for a cache bootstrap
-                qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2]
+                qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2] and fmts[3] != D.FMT_BF16
                 self.launches += 11 - (1 if self.fuse_refresh else 0) - (2 if qkv1 else 0) + (2 if first else 0)
             rec.linear_flops += flops
             rec.fmts.append(None if d == L.TDC_DECIDE_SKIP else fmts)

@@ -106,6 +106,10 @@ def dmpq_concat_weights(pws: list) -> tuple:
         raise ValueError("dmpq_concat_weights: equal k, n % 128 == 0 and one Hadamard setting required")
     has_bias = all(p.bias is not None for p in pws)
     has_bf16 = all(p.bf16_w is not None for p in pws)
+    if not has_bias and any(p.bias is not None for p in pws):
+        raise ValueError("dmpq_concat_weights: bias on some layers but not on others")
+    if not has_bf16 and any(p.bf16_w is not None for p in pws):
+        raise ValueError("dmpq_concat_weights: bf16_w kept on some layers but not on others")
     n = sum(p.n for p in pws)
     codes = torch.cat([p.fp4_codes for p in pws])
     sf = torch.cat([p.fp4_sf for p in pws])
@@ -178,7 +182,8 @@ class QuantAct:
     def bf16(cls, X: torch.Tensor):
         """The unquantised activation itself, for the BF16 (PDR fallback) GEMM path."""
         _check_dev(X, "X", torch.bfloat16)
-        assert X.is_contiguous()
+        if not X.is_contiguous():   # the BF16 GEMM's A tensor map has row stride k (include/dmpq.h dmpq_act)
+            raise ValueError("a BF16 activation must be dense (row stride k)")
         m, k = X.shape
         a = cls(FMT_BF16, m, k, X)
         a.c = L.Act(FMT_BF16, m, k, X.data_ptr(), None, None, None)

@@ -128,3 +128,31 @@ def test_purify_matches_oracle(L, orc):
         got = dmpq.dmpq_purify(fm, ratios, ps, 25.0)
         assert got == [orc.purify_route(f, r, ps, 25.0) for f, r in zip(fm, ratios)]
     assert dmpq.dmpq_purify([1, 1], None, True) == [0, 0]
+
+
+def test_predict_l2_metric_matches_oracle(L, orc):
+    """dmpq_predict with the L2 Gamma variant (DMPQ_GAMMA_L2, R1) against the oracle's
+    gamma_from_stats(metric="l2") and Eq. 7 routing; SPEC rel_l2 examples via the statistics."""
+    from paper_2603_18742_b200 import dmpq
+    rng = np.random.default_rng(4)
+    taus = [0.015, 0.01, 0.0043, 0.02, 0.0075, 0.012]
+    for trial in range(2000):
+        st = list(rng.uniform(0, 1, 7))
+        st[3] = st[2] / rng.uniform(0.002, 0.05) ** 2 if trial % 50 else 0.0
+        t = int(rng.integers(0, 5))
+        ps = bool(rng.integers(0, 2))
+        fmts, gamma, rc = dmpq.dmpq_predict(st, taus, t, ps, metric=L.GAMMA_L2)
+        g_or = orc.gamma_from_stats(st, "l2")
+        assert fmts == orc.route_block(g_or, taus, t, ps)
+        if t > 0 and not ps and g_or is not None:
+            assert gamma == pytest.approx(g_or, rel=1e-15)
+        if st[3] == 0.0 and t > 0 and not ps:
+            assert rc == L.DMPQ_EZERONORM
+    # ref [3, 4] vs other [0, 0]: sum d^2 = 25, sum x^2 = 25 -> Gamma_L2 = 1 (S:49) -> INT8 at tau 0.015
+    fmts, gamma, _ = dmpq.dmpq_predict([7, 7, 25, 25, 0, 0, 0], [0.015, 2.0], 3, False, metric=L.GAMMA_L2)
+    assert gamma == 1.0 and fmts == [orc.FMT_INT8, orc.FMT_NVFP4]
+    # the same statistics under L1 give Gamma = 1 as well; a case where they differ: L1 0.5, L2 1/sqrt(2)
+    st = [1.0, 2.0, 1.0, 2.0, 0, 0, 0]
+    assert dmpq.dmpq_predict(st, [0.6], 3, False)[1] == 0.5
+    assert dmpq.dmpq_predict(st, [0.6], 3, False, metric=L.GAMMA_L2)[1] == pytest.approx(2 ** -0.5, rel=1e-15)
+    assert dmpq.dmpq_predict(st, [0.6], 3, False, metric=L.GAMMA_L2)[0] == [orc.FMT_INT8]

@@ -158,3 +158,79 @@ def test_fullsize_tdc_nvfp4_cache(D, orc):
     np.testing.assert_allclose(s[:4], st[:4], rtol=4.2e-7)
     np.testing.assert_allclose(s[4:], st[4:], rtol=1e-12)
     assert np.array_equal(synth.bits(out.cpu()), orc.tdc_skip_nvfp4(synth.bits(xo), cn, sn, g_new.item()))
+
+
+@pytest.mark.parametrize("which", ["nvfp4", "int8", "both"])
+def test_fullsize_layernorm_hadamard_no_h(D, orc, which):
+    """The exact quantizer launches of the bench's attention / FFN1 inputs at full size: LN +
+    Hadamard without the h output, formats fixed at compile time (quant_had_kernel<LN,!PDR,!WH,FMT>),
+    sampled rows bit-exact against the oracle on the LN rows of the h-writing variant; the tensor
+    amax over all rows."""
+    k = 3072
+    x = synth.dit_activation(M, k, seed=k + 2)
+    xd = x.cuda()
+    h = torch.empty(M, k, dtype=torch.bfloat16, device="cuda")
+    a_h = D.QuantAct.empty(D.FMT_INT8, M, k, "cuda")
+    D.dmpq_quantize_act(xd, out_i8=a_h, layernorm=True, h_out=h, hadamard=True)
+    g = torch.tensor([0.02], device="cuda")
+    a8 = D.QuantAct.empty(D.FMT_INT8, M, k, "cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, M, k, "cuda", g=g)
+    amax = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(xd, out_i8=a8 if which != "nvfp4" else None, out_fp4=a4 if which != "int8" else None,
+                        amax_out=amax, layernorm=True, hadamard=True)
+    torch.cuda.synchronize()
+    src = synth.bits(h.cpu())
+    y_all = orc.fht128(orc.bf16_to_f32(src).reshape(M, k))
+    assert amax.item() == float(np.abs(y_all).max())
+    c8_all, s8_all = a8.codes.cpu().numpy(), a8.row_scale.cpu().numpy()
+    c4_all, sf4 = a4.codes.cpu().numpy(), orc.sf_unswizzle(a4.sf.cpu().numpy(), M, k)
+    for r in sample_rows(M, n=40, seed=2):
+        y = y_all[r:r + 1]
+        if which != "nvfp4":
+            c8, s8 = orc.int8_quantize_f32(y)
+            assert np.array_equal(c8_all[r:r + 1], c8) and s8_all[r] == s8[0], r
+        if which != "int8":
+            c4, s4 = orc.nvfp4_quantize_f32(y, 0.02)
+            assert np.array_equal(c4_all[r:r + 1], c4) and np.array_equal(sf4[r:r + 1], s4), r
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_fullsize_qkv_concat_sampled(D, orc, fmt):
+    """The bench's most frequent GEMM: Q | K | V side by side (N = 9216, K = 3072, M = 35,552,
+    Hadamard-packed, per-column NVFP4 g_w) on sampled rows against the oracle's GEMM with each
+    layer's own packed weights and g_w (INT8 bit-exact, NVFP4 fp32 rel-L2 <= 1e-5)."""
+    H = 3072
+    packs, pks = [], []
+    for j in range(3):
+        w, b = synth.linear_weight_device(H, H, seed=900 + j, device="cuda")
+        packs.append(D.dmpq_pack_weights(w, b, hadamard=True))
+        pks.append((orc.pack_weights_hadamard(synth.bits(w.cpu())), b.cpu().numpy()))
+    assert len({p.fp4_g.item() for p in packs}) == 3
+    cat, _ = D.dmpq_concat_weights(packs)
+    x = synth.dit_activation(M, H, seed=77)
+    g = torch.tensor([0.02], device="cuda")
+    a = D.QuantAct.empty(fmt, M, H, "cuda", g=g if fmt == 1 else None)
+    D.dmpq_quantize_act(x.cuda(), out_fp4=a if fmt == 1 else None, out_i8=a if fmt == 0 else None, hadamard=True)
+    y32 = torch.empty(M, 3 * H, dtype=torch.float32, device="cuda")
+    y = torch.empty(M, 3 * H, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a, cat, Y=y, Y32=y32)
+    torch.cuda.synchronize()
+    codes = a.codes.cpu().numpy()
+    if fmt == 1:
+        sfa = orc.sf_unswizzle(a.sf.cpu().numpy(), M, H)
+    else:
+        s8 = a.row_scale.cpu().numpy()
+    rows = sample_rows(M, n=6, seed=3)
+    for j, (pk, bias) in enumerate(pks):
+        assert packs[j].fp4_g.item() == pk["fp4_g"]
+        for r in rows:
+            got = y32[r, j * H:(j + 1) * H].cpu().numpy()
+            assert torch.equal(y[r, j * H:(j + 1) * H].cpu(), torch.from_numpy(got).to(torch.bfloat16))
+            if fmt == 0:
+                _, ref = orc.gemm_int8(codes[r:r + 1], s8[r:r + 1], pk["i8_codes"], pk["i8_scale"], bias)
+                assert np.array_equal(got, ref[0]), (j, r)
+            else:
+                ref = orc.gemm_nvfp4(codes[r:r + 1], sfa[r:r + 1], 0.02, pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"],
+                                     bias)[0]
+                err = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
+                assert err <= 1e-5, (j, r, err)

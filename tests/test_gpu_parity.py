@@ -175,13 +175,29 @@ def test_gemm_gated_residual(D, orc, fmt, m, n, k):
     torch.cuda.synchronize()
     assert torch.equal(y32_tma.cpu(), y32_lane.cpu())
     assert torch.equal(y.cpu(), y32_tma.cpu().to(torch.bfloat16))
+    gate64 = gate.cpu().numpy().astype(np.float64)[None, :]
+    res64 = res.cpu().float().numpy().astype(np.float64)
+    got = y32_tma.cpu().numpy().astype(np.float64)
     if fmt == 0:
         _, y_lin = orc.gemm_int8(a.codes.cpu().numpy(), a.row_scale.cpu().numpy(), pw.i8_codes.cpu().numpy(),
                                  pw.i8_scale.cpu().numpy(), b.numpy())
-        ref = (gate.cpu().numpy().astype(np.float64)[None, :] * y_lin.astype(np.float64)
-               + res.cpu().float().numpy().astype(np.float64))
-        got = y32_tma.cpu().numpy().astype(np.float64)
+        ref = gate64 * y_lin.astype(np.float64) + res64
         assert np.all(np.abs(got - ref) <= np.abs(ref) * 2.0 ** -23 + 1e-30)
+    else:
+        # NVFP4: the plain GEMM's fp32 output is within rel-L2 1e-5 of the oracle's fp64 accumulation
+        # over the same codes, and the gated-residual output is fma(gate, y, res) of exactly that y
+        # (one fp32 rounding of the exact value)
+        y_plain = torch.empty(m, n, dtype=torch.float32, device="cuda")
+        D.dmpq_gemm(a, pw, Y32=y_plain)
+        torch.cuda.synchronize()
+        y64 = orc.gemm_nvfp4(a.codes.cpu().numpy(), orc.sf_unswizzle(a.sf.cpu().numpy(), m, k), g.item(),
+                             pw.fp4_codes.cpu().numpy(), orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k),
+                             pw.fp4_g.item(), b.numpy())
+        yp = y_plain.cpu().numpy().astype(np.float64)
+        assert rel_l2(yp, y64) <= 1e-5
+        ref = gate64 * yp + res64
+        assert np.all(np.abs(got - ref) <= np.abs(ref) * 2.0 ** -23 + 1e-30)
+        assert rel_l2(got - res64, gate64 * y64) <= 1e-5
 
 
 @pytest.mark.parametrize("fmt,m,k,had", [(0, 300, 256, False), (1, 300, 256, False), (1, 1029, 512, True),
@@ -517,3 +533,70 @@ def test_pdr_statistics(D, orc, m, k, had):
     assert tot.item() == pytest.approx(float(rs[0].cpu().numpy().astype(np.float64).sum()), rel=1e-12)
     r_gpu = ain.item() / (tot.item() / (m * k))
     assert r_gpu == pytest.approx(orc.outlier_ratio(synth.bits(x)), rel=1e-5)
+
+
+@pytest.mark.parametrize("k", [3072, 12288])
+@pytest.mark.parametrize("which", ["nvfp4", "int8", "both"])
+def test_quantize_hadamard_layernorm_no_h(D, orc, k, which):
+    """The bench's LayerNorm + Hadamard quantizer instantiations (no h output, output formats fixed
+    at compile time: quant_had_kernel<LN, !PDR, !WH, FMT 1 / 2 / 3>): codes, scales, row scales and
+    amax equal the oracle's FP32 FHT + quantizers applied to the LN rows of the h-writing variant."""
+    m = 1029
+    x = synth.dit_activation(m, k, seed=k + 31)
+    xd = x.cuda()
+    h = torch.empty(m, k, dtype=torch.bfloat16, device="cuda")
+    a_h = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    D.dmpq_quantize_act(xd, out_i8=a_h, layernorm=True, h_out=h, hadamard=True)
+    g = torch.tensor([0.004], device="cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, m, k, "cuda", g=g)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    amax = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(xd, out_i8=a8 if which != "nvfp4" else None, out_fp4=a4 if which != "int8" else None,
+                        amax_out=amax, layernorm=True, hadamard=True)
+    torch.cuda.synchronize()
+    y = orc.fht128(orc.bf16_to_f32(synth.bits(h.cpu())).reshape(m, k))
+    assert amax.item() == float(np.abs(y).max())
+    if which != "nvfp4":
+        c8, s8 = orc.int8_quantize_f32(y)
+        assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+        assert np.array_equal(a8.codes.cpu().numpy(), c8)
+    if which != "int8":
+        c4, s4 = orc.nvfp4_quantize_f32(y, 0.004)
+        assert np.array_equal(orc.sf_unswizzle(a4.sf.cpu().numpy(), m, k), s4)
+        assert np.array_equal(a4.codes.cpu().numpy(), c4)
+
+
+@pytest.mark.parametrize("had", [True, False])
+def test_graph_replay_equals_eager(D, had):
+    """The bench's headline pass replays one CUDA graph per (block, decision, formats) pattern.
+    Six timesteps of a two-block stack replayed from graphs equal the same steps launched eagerly
+    bit for bit: outputs of every step, delta caches, FP64 statistics, global scales, decisions."""
+    from paper_2603_18742_b200.block import DiTStack
+    M, H, F, T = 1000, 128, 512, 6
+    A, B = synth.trajectory_basis(M, H, seed=5)
+    xs = [synth.trajectory_input(A, B, t, 50).cuda() for t in range(T)]
+    runs = []
+    for graphs in (False, True):
+        stack = DiTStack(2, H, F, M, "cuda", seed=4, gate_scales=[0.008, 0.012], hadamard=had,
+                         tdc_cfg=(0.001, 0.02, 2))
+        stack.use_graphs = graphs
+        outs, stats = [], []
+        for t in range(T):
+            outs.append(stack.step(xs[t], t).clone())
+            stats.append(stack.end_step(t).copy())
+        torch.cuda.synchronize()
+        runs.append(dict(outs=[o.cpu() for o in outs], stats=stats, delta=[d.cpu() for d in stack.delta],
+                         g=stack.g_table.cpu(), dec=[r.decisions for r in stack.records],
+                         fmts=[r.fmts for r in stack.records], graphs=sum(len(g) for g in stack.graphs)))
+    e, g = runs
+    assert g["graphs"] > 0 and e["graphs"] == 0
+    assert e["dec"] == g["dec"] and e["fmts"] == g["fmts"]
+    assert any(d == 1 for ds in e["dec"] for d in ds), "the trajectory should skip at least once"
+    assert {f for fs in e["fmts"] for ff in fs if ff for f in ff} >= {0, 1}, "both formats should run"
+    for a, b in zip(e["outs"], g["outs"]):
+        assert torch.equal(a, b)
+    for a, b in zip(e["stats"], g["stats"]):
+        assert np.array_equal(a, b)
+    for a, b in zip(e["delta"], g["delta"]):
+        assert torch.equal(a, b)
+    assert torch.equal(e["g"], g["g"])

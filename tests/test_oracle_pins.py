@@ -624,3 +624,113 @@ def test_cache_skip_is_codec_composition(orc):
     assert np.all(np.abs(dq.astype(np.float64) - d) <= eff)      # one E2M1 step at most
     ref = (xi.float() + torch.tensor(dq)).to(torch.bfloat16)
     assert np.array_equal(orc.tdc_skip_nvfp4(synth.bits(xi), cn, sn, g), synth.bits(ref))
+
+
+# ---------------------------------------------------------------------------- round-2 pins
+# (functions the round-1 pins only used as checkers; each pinned to an independent source)
+
+def test_amax_bf16_vs_numpy(orc):
+    """Tensor amax max|x| (R3's delayed global scale) against numpy's reduction over the widened
+    bf16 values; rows whose largest magnitude is negative, signed zeros and huge/tiny values."""
+    rng = np.random.default_rng(21)
+    cases = [rng.standard_normal((37, 64)).astype(np.float32),
+             np.array([[0.5, -7.25, 3.0, -0.0]], np.float32),           # max magnitude is negative
+             np.array([[-0.0, -0.0, 0.0]], np.float32),                 # all zeros -> 0
+             np.array([[1e-38, -3e-39, 2e-40]], np.float32),            # bf16 subnormals
+             np.array([[-3.0e38, 1.0, 2.5e38]], np.float32)]
+    for c in cases:
+        b = bf16_bits(c)
+        assert orc.amax_bf16(b) == float(np.abs(bf16_vals(b)).max())
+    assert orc.amax_bf16(bf16_bits([[-7.25, 7.0]])) == 7.25
+
+
+def test_global_scale_floor_and_division(orc):
+    """g = max(fl(amax / div), FLT_MIN) (R3): IEEE single division (numpy float32) above the
+    floor; amax 0 and quotients below FLT_MIN (subnormal or zero) give exactly FLT_MIN."""
+    flt_min = float(np.finfo(np.float32).tiny)
+    for div in (1344.0, 2688.0):
+        assert orc.global_scale(0.0, div) == flt_min
+        assert orc.global_scale(1e-40, div) == flt_min          # denormal amax
+        assert orc.global_scale(flt_min, div) == flt_min        # quotient underflows below the floor
+        assert orc.global_scale(div, div) == 1.0
+        rng = np.random.default_rng(int(div))
+        for a in np.concatenate([10.0 ** rng.uniform(-30, 30, 2000), [448.0 * 6, 1.0, 3.0]]).astype(np.float32):
+            q = np.float32(a) / np.float32(div)
+            assert orc.global_scale(float(a), div) == float(max(q, np.float32(flt_min)))
+
+
+def test_gamma_l2_spec_examples(orc):
+    """Eq. 4's normalized L2 distance as the L2 variant of Gamma (R1), from the statistics the
+    refresh produces: SPEC rel_l2 examples and the identity case."""
+    ex = GOLDEN["rel_l2_examples"]["cases"]
+    for case in ex:
+        _, st = orc.block_stats(bf16_bits(case["ref"]), bf16_bits(case["other"]))
+        want = math.sqrt(2.0) if case["value"] == "sqrt2" else case["value"]
+        assert orc.gamma_from_stats(st, "l2") == pytest.approx(want, rel=1e-15)
+    x = bf16_bits([0.5, -2.0, 3.0])
+    _, st = orc.block_stats(x, x)
+    assert orc.gamma_from_stats(st, "l2") == 0.0
+    _, st = orc.block_stats(bf16_bits([0.0, 0.0]), bf16_bits([1.0, 1.0]))
+    assert orc.gamma_from_stats(st, "l2") is None                  # zero-norm reference (S:47, S:38)
+    # L1 and L2 differ where they should: ref [1, 1], other [2, 1] -> L1 0.5, L2 1/sqrt(2)
+    _, st = orc.block_stats(bf16_bits([1.0, 1.0]), bf16_bits([2.0, 1.0]))
+    assert orc.gamma_from_stats(st, "l1") == 0.5
+    assert orc.gamma_from_stats(st, "l2") == pytest.approx(1 / math.sqrt(2), rel=1e-15)
+
+
+# Scale-factor placement of the tcgen05 block-scaled MMA, written from the hardware's data path
+# rather than from the oracle's formula: a 128-row x 4-scale-column chunk (128 rows x 64 K elements
+# at scale_vec::4X) is one 512-byte smem atom, copied to TMEM by tcgen05.cp .32x128b.warpx4 as 32
+# rows of 16 bytes, row l going to TMEM lane l of every 32-lane quarter q; the MMA row m = 32 q + l
+# reads its four K-block scales from bytes 4q .. 4q+3 of that 16-byte row. Atoms are stored
+# K-fastest (all K chunks of a 128-row tile, then the next 128 rows). Each entry: (r, c, k) -> byte.
+SF_HAND_TABLE = [
+    ((0, 0, 64), 0),            # first scale of the first atom
+    ((0, 3, 64), 3),            # 4th K-block of row 0: same 16-byte row, byte 3
+    ((1, 0, 64), 16),           # row 1 -> smem row 1 (lane 1 of quarter 0)
+    ((31, 0, 64), 496),         # last smem row
+    ((32, 0, 64), 4),           # row 32 = lane 0 of quarter 1 -> bytes 4..7 of smem row 0
+    ((33, 2, 64), 22),          # lane 1, quarter 1, K-block 2: 16 + 4 + 2
+    ((96, 1, 64), 13),          # quarter 3: bytes 12..15 of smem row 0
+    ((127, 3, 64), 511),        # last byte of the atom
+    ((128, 0, 64), 512),        # second 128-row tile (k = 64: one atom per row tile)
+    ((0, 4, 128), 512),         # k = 128: the second K chunk of row tile 0 comes next (K-fastest)
+    ((128, 0, 128), 1024),      # then row tile 1
+    ((128, 5, 128), 1537),      # row tile 1, K chunk 1, K-block 1
+    ((200, 117, 1920), 30345),  # k = 1920: 30 K chunks per row tile; (1*30 + 29)*512 + 8*16 + 2*4 + 1
+]
+
+
+def test_sf_offset_hand_table(orc):
+    for (r, c, k), byte in SF_HAND_TABLE:
+        assert orc.sf_offset(r, c, k) == byte, (r, c, k)
+        # the gather used by the tests agrees with the table too
+        dev = np.zeros(orc.sf_swizzled_bytes(r + 1, k), np.uint8)
+        dev[byte] = 0x5A
+        logical = orc.sf_unswizzle(dev, r + 1, k)
+        assert logical[r, c] == 0x5A and int((logical == 0x5A).sum()) == 1
+
+
+def test_sf_offset_hierarchical_layout(orc):
+    """The same placement from CuTe's hierarchical layout notation of the SF atom,
+    Shape ((32, 4), (16, 4)) : Stride ((16, 4), (0, 1)) over (row, K element) of a 128 x 64 tile,
+    evaluated by a generic colexicographic shape/stride evaluator, tiled K-fastest."""
+    def evaluate(coord, shape, stride):
+        off = 0
+        for x, sh, st in zip(coord, shape, stride):
+            if isinstance(sh, tuple):
+                for s_, t_ in zip(sh, st):
+                    off += (x % s_) * t_
+                    x //= s_
+            else:
+                off += x * st
+        return off
+    shape, stride = ((32, 4), (16, 4)), ((16, 4), (0, 1))
+    for k in (64, 192, 1920, 3072):
+        kc4 = k // 64
+        for r in (0, 5, 31, 32, 77, 127, 128, 300, 1000):
+            for c in sorted({0, 1, 3, 4, k // 16 - 1, (k // 16) // 2}):
+                ke = c * 16 + 7          # any K element of the 16-element block
+                inner = evaluate(((r % 128), ke % 64), shape, stride)
+                atom = (r // 128) * kc4 + (ke // 64)
+                assert orc.sf_offset(r, c, k) == atom * 512 + inner, (r, c, k)
