@@ -18,8 +18,8 @@ wrapped by the paper's per-step control:
     Gamma_{t-1} (dmpq_predict), NVFP4 global scales from the previous step's amax
     (delayed policy, R3).
 Token sharding (shard.py): each rank owns a contiguous row range; the per-step
-statistics are combined across ranks with one slot-packed SUM all-reduce (stats)
-and one MAX all-reduce (amax), after which every rank takes identical decisions.
+statistics and maxima are combined across ranks with ONE slot-packed SUM all-reduce
+(an exact all-gather), after which every rank takes identical decisions.
 """
 from __future__ import annotations
 
@@ -32,7 +32,7 @@ import torch
 from . import _lib as L
 from . import dmpq as D
 from . import synth
-from .shard import exchange
+from .shard import SlotBuffer, combine_host, exchange_device
 
 LAYERS = ("q", "k", "v", "o", "ffn1", "ffn2")
 N_STATS = L.STATS_LEN + 4      # per block: 7 TDC/predictor sums + sum|x| of the 4 layer inputs (PDR, R15)
@@ -166,7 +166,10 @@ class DiTStack:
         world = 1 if group is None else torch.distributed.get_world_size(group)
         self.world = world
         self.rank = 0 if group is None else torch.distributed.get_rank(group)
-        self.stats_slots = torch.zeros(world, n_blocks, N_STATS, dtype=torch.float64, device=self.device)
+        # the per-step exchange buffer: this rank's FP64 statistics and fp32 maxima in its own slot,
+        # one SUM all-reduce per step (shard.py)
+        self.slots = SlotBuffer(world, self.rank, n_blocks * N_STATS, self.amax_all.numel(), self.device)
+        self.stats_slots = self.slots.stats.view(world, n_blocks, N_STATS)
         self.ratio = [None] * n_blocks          # PDR outlier ratio per slot from the block's last compute
         self.x_buf = [torch.empty(m_local, H, dtype=torch.bfloat16, device=self.device) for _ in range(2)]
         self.tdc = [D.tdc_new_state() for _ in range(n_blocks)]
@@ -357,7 +360,7 @@ class DiTStack:
         (a view of an internal buffer). Call end_step(t) afterwards."""
         rec = StepRecord(t)
         self.amax.zero_()
-        self.stats_slots.zero_()
+        self.slots.zero_()
         graphs = self.use_graphs and not self.timing and self.capture is None
         if graphs and x0.data_ptr() != self.x_in0.data_ptr():
             self.x_in0.copy_(x0)
@@ -410,17 +413,17 @@ class DiTStack:
         return x_in
 
     def end_step(self, t: int):
-        """Per-step exchange + host decisions: combine the statistics of all ranks
-        (slot-packed SUM all-reduce = exact all-gather; MAX all-reduce for amax), copy
-        them to the host once, update TDC (Eq. 10) and the NVFP4 global scales (R3)."""
+        """Per-step exchange + host decisions: combine the statistics and maxima of all ranks
+        (one slot-packed SUM all-reduce = exact all-gather), copy them to the host once,
+        update TDC (Eq. 10) and the NVFP4 global scales (R3)."""
         with self._ev("exchange"):
             if self.pdr:   # per-slot sum|x| of this rank's rows -> its stats slot (FP64, fixed order)
                 D.dmpq_outlier_reduce(self.row_abs, self.pdr_sums)
                 self.stats_slots[self.rank, :, L.STATS_LEN:] = self.pdr_sums.view(self.nb, N_SLOTS)
                 self.launches += 1
-            if self.group is not None and self.world > 1:
-                torch.distributed.all_reduce(self.stats_slots, op=torch.distributed.ReduceOp.SUM, group=self.group)
-                torch.distributed.all_reduce(self.amax_all, op=torch.distributed.ReduceOp.MAX, group=self.group)
+            # one SUM all-reduce of the slot buffer (statistics + maxima): every rank then holds
+            # every rank's partial sums and the global maxima
+            exchange_device(self.slots, self.amax_all, self.group)
             # next step's NVFP4 global scales from the (all-rank) amax of this step (R3)
             D.dmpq_global_scale(self.amax[0].view(-1), 1344.0, self.g_table.view(-1))
             self.launches += 1
@@ -428,7 +431,7 @@ class DiTStack:
                 D.dmpq_global_scale(self.delta_amax, 1344.0, self.g_delta)
                 self.launches += 1
         # the D2H copy inside synchronises the stream (one exchange per step)
-        stats = exchange(self.stats_slots, self.amax, None, 1)
+        stats = combine_host(self.slots).reshape(self.nb, N_STATS)
         if self.pdr:
             amax_in = self.amax[1].cpu().numpy().astype(np.float64)
         rec = self.records[-1]

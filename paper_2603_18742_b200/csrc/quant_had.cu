@@ -110,12 +110,18 @@ struct Seg8 {
     }
 };
 
-// |x| maximum of 16 values (8 packed pairs), exact
+// three-input maximum (FMNMX3 on sm_100; |x| operands fold into the instruction's modifiers)
+__device__ __forceinline__ float hmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// |x| maximum of 16 values (8 packed pairs), exact: 8 FMNMX3
 __device__ __forceinline__ float habsmax8p(const f2* y) {
-    float m = 0.0f;
+    float m = hmax3(fabsf(f2lo(y[0])), fabsf(f2hi(y[0])), fabsf(f2lo(y[1])));
 #pragma unroll
-    for (int e = 0; e < 8; ++e) m = fmaxf(m, fmaxf(fabsf(f2lo(y[e])), fabsf(f2hi(y[e]))));
-    return m;
+    for (int e = 1; e < 7; ++e) m = hmax3(m, fabsf(f2hi(y[e])), fabsf(f2lo(y[e + 1])));
+    return hmax3(m, fabsf(f2hi(y[7])), 0.0f);
 }
 
 // four int8 codes RNE(fl(y * r)) of y = (y01.lo, y01.hi, y23.lo, y23.hi), |fl(y r)| < 2^22:
@@ -233,6 +239,16 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
             Y[32 + 4 * u + 3] = bf16x2_to_f2(v.w);
         }
 
+        // the row set is in registers: release buffer b right away and (thread 0, once every warp
+        // has released it) refill it with row set it + nbuf, so the next nbuf row sets are in
+        // flight during this one's whole computation
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
+        if (tid == 0 && it + nbuf < iters) {
+            mbar_wait(bar0 + 8 * (nbuf + b), ph);
+            issue(b, set + nbuf * (int)gridDim.x);
+        }
+
         if constexpr (LN) {
             // h = bf16(fl(x rstd - fl(mean rstd))) (glue, R13): one pass of packed raw sums
             // S1 = sum x, S2 = sum x^2 (FP32), mean = S1/k, var = max(S2/k - mean^2, 0).
@@ -321,21 +337,11 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
             }
         }
 
-        // the row set is in registers: release buffer b and (thread 0, once every warp has
-        // released it) refill it with row set it + nbuf, so nbuf row sets stay in flight
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
-        if (tid == 0 && it + nbuf < iters) {
-            mbar_wait(bar0 + 8 * (nbuf + b), ph);
-            issue(b, set + nbuf * (int)gridDim.x);
-        }
-
         // per-16-block |y| maxima and this thread's maximum
         float a[8];
 #pragma unroll
         for (int bb = 0; bb < 8; ++bb) a[bb] = habsmax8p(&Y[8 * bb]);
-        const float tmax = cvalid ? fmaxf(fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])), fmaxf(fmaxf(a[4], a[5]), fmaxf(a[6], a[7])))
-                                  : 0.0f;
+        const float tmax = cvalid ? hmax3(hmax3(a[0], a[1], a[2]), hmax3(a[3], a[4], a[5]), fmaxf(a[6], a[7])) : 0.0f;
         my_amax = fmaxf(my_amax, tmax);
 
         if (want_fp4 && live) {

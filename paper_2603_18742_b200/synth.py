@@ -84,6 +84,25 @@ def linear_weight_device(n: int, k: int, seed: int, device):
     return w, b
 
 
+def dit_activation_device(m: int, k: int, seed: int, device, outlier_frac: float = 0.005,
+                          tail_frac: float = 0.01) -> torch.Tensor:
+    """Device-side variant of dit_activation (same recipe, different random stream) for the large
+    bench inputs (the C2 sweep's 64K x 1920 rows), where CPU generation is slow."""
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    x = torch.randn(m, k, generator=g, device=device)
+    x *= torch.exp(0.5 * torch.randn(m, 1, generator=g, device=device))
+    n_out = max(1, int(round(outlier_frac * k)))
+    ch = torch.randperm(k, generator=g, device=device)[:n_out]
+    x[:, ch] *= 10 + 40 * torch.rand(n_out, generator=g, device=device)
+    if tail_frac > 0:
+        mask = torch.rand(m, k, generator=g, device=device) < tail_frac
+        z = torch.randn(m, k, generator=g, device=device)
+        chi = sum(torch.randn(m, k, generator=g, device=device) ** 2 for _ in range(4))
+        x = torch.where(mask, z / torch.sqrt(chi / 4), x)
+    return x.to(torch.bfloat16)
+
+
 def trajectory_basis(m: int, h: int, seed: int, device=None):
     """Two bf16-valued basis tensors A, B [m, h] for the synthetic PF-ODE-like
     block-0 input X_t = cos(theta_t) A + sin(theta_t) B (a smooth, locally

@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2603_18742_b200.shard import exchange, shard_rows
+from paper_2603_18742_b200.shard import SlotBuffer, exchange, shard_rows
 
 
 def test_shard_rows_partition():
@@ -54,13 +54,15 @@ def _worker(rank, world, port, M, H, nb, q):
     import oracle
     from paper_2603_18742_b200 import dmpq as D, synth
     r0, r1 = shard_rows(M, world, rank)
-    slots = torch.zeros(world, nb, 7, dtype=torch.float64)
+    slots = SlotBuffer(world, rank, nb * 7, nb * 4, "cpu")
+    stats_view = slots.stats.view(world, nb, 7)
     amax = torch.zeros(nb, 4, dtype=torch.float32)
     for b, (xi, xo, dp) in enumerate(_inputs(M, H, nb)):
         _, st = oracle.block_stats(synth.bits(xi[r0:r1]), synth.bits(xo[r0:r1]), synth.bits(dp[r0:r1]))
-        slots[rank, b] = torch.from_numpy(st)
+        stats_view[rank, b] = torch.from_numpy(st)
         amax[b, 0] = oracle.amax_bf16(synth.bits(xi[r0:r1]))
-    stats = exchange(slots, amax, dist.group.WORLD, world)
+        amax[b, 1] = oracle.amax_bf16(synth.bits(xo[r0:r1]))
+    stats = exchange(slots, amax, dist.group.WORLD).reshape(nb, 7)
     taus = [D.dmpq_derive_tau(0.1 * (1 + j / 2), 0.001, 0.0025) for j in range(6)]
     fmts = [D.dmpq_predict(stats[b], taus, 3, False)[0] for b in range(nb)]
     q.put((rank, stats, amax.numpy().copy(), fmts))
@@ -90,4 +92,5 @@ def test_exchange_gloo_world2(orc):
         _, st = orc.block_stats(synth.bits(xi), synth.bits(xo), synth.bits(dp))
         np.testing.assert_allclose(res[0][1][b], st, rtol=1e-12)
         assert res[0][2][b, 0] == orc.amax_bf16(synth.bits(xi))
+        assert res[0][2][b, 1] == orc.amax_bf16(synth.bits(xo))
         assert res[0][3][b] == orc.route_block(orc.gamma_from_stats(st), taus, 3, False)
