@@ -457,7 +457,8 @@ def run_ours(args):
     peaks, peak_kind = load_peaks()
 
     model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
-                     pdr=args.pdr, m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh)
+                     pdr=args.pdr, m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh,
+                     int8_cast=args.int8_cast)
     # block-0 input trajectory basis: ONE seeded global [M x H] input, of which this rank takes its
     # contiguous row shard -- every world size solves the same problem (same mix, same decisions)
     A, B = synth.trajectory_basis(M, H, seed=1000 + args.seed, device=dev)
@@ -555,7 +556,7 @@ def run_ours(args):
     brk = model.breakdown_s()
     breakdown = {"gemm": sum(v[0] for v in gemm_t.values()) / args.steps * 1e3,
                  "quantize": brk["quantize"] / args.steps * 1e3, "tdc": brk["tdc"] / args.steps * 1e3,
-                 "exchange": brk["exchange"] / args.steps * 1e3}
+                 "exchange": brk["exchange"] / args.steps * 1e3, "int8_cast": brk["cast"] / args.steps * 1e3}
     breakdown["host_gaps_and_other"] = elapsed_b / args.steps * 1e3 - sum(breakdown.values())
     breakdown["pass"] = "eager replay of the timed steps with per-launch CUDA events"
 
@@ -679,7 +680,7 @@ def run_ours(args):
                    "device_map": os.environ.get("DMPQ_DEVICE_MAP", "one GPU per rank"),
                    "input": "one seeded global input; each rank takes its contiguous row shard", "l2": "inputs larger than L2 (multi-GB working set per step)",
                    "cuda_graphs": not args.no_graphs, "tdc_refresh": "fused in the FFN2 GEMM epilogue" if model.fuse_refresh else "own kernel",
-                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr,
+                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr, "int8_weight_cast": args.int8_cast,
                    "delta_cache": {"format": "nvfp4" if args.cache_nvfp4 else "bf16",
                                    "bytes_per_rank": sum(d.nbytes() if args.cache_nvfp4 else d.numel() * 2
                                                          for d in model.delta)},
@@ -746,6 +747,8 @@ def main():
     ap.add_argument("--fused-refresh", action="store_true", help="run the TDC refresh in the FFN2 GEMM epilogue "
                     "instead of its own kernel (SURVEY NEXT-2; measured slower, DESIGN.md 5.7c)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
+    ap.add_argument("--int8-cast", action="store_true", help="NVFP4-only weight residency, INT8 codes cast on the fly "
+                    "per INT8 GEMM (P:184, NEXT-4b)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs --warmup >= 3", file=sys.stderr)

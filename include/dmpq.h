@@ -98,6 +98,8 @@ typedef struct {
                               layers packed side by side along n (e.g. Q, K, V over the same input)
                               keep their own per-tensor scales; the NVFP4 epilogue then uses
                               fl(g_a * fp4_g_col[n]) per column, bit-identical to separate GEMMs */
+    float* i8_rcp;         /* [n] or NULL: r_w[n] = fl(127 / max_k|W^|) (0 for a zero row), written by the
+                              pack when non-NULL; lets dmpq_cast_int8 rebuild the INT8 codes on the fly */
 } dmpq_weights;
 
 /* A quantized activation tensor, as written by dmpq_quantize_act. */
@@ -124,6 +126,20 @@ typedef struct {
 dmpq_status dmpq_pack_weights(const uint16_t* W, int n, int k, dmpq_weights* out, dmpq_stream_t s);
 
 #define DMPQ_PACK_HADAMARD 1u  /* rotate every row by the block FHT first (offline half of P:187's smoothing, R14) */
+
+/* With out->i8_rcp != NULL the pack also writes r_w; out->i8_codes may then be NULL (NVFP4-only
+ * residency: the INT8 form is rebuilt per GEMM by dmpq_cast_int8). out->i8_scale is always written. */
+
+/* On-the-fly NVFP4 -> INT8 weight cast ("all weights are quantized to NVFP4 offline ... for
+ * layers routed to INT8, the NVFP4 weights are cast to INT8 on-the-fly"; R7, NEXT-4b): writes the
+ * INT8 codes of W into i8_out (device, [W->n x W->k], row-major, caller-owned scratch, 16-byte
+ * aligned) from W's NVFP4 codes / scales / g_w and r_w (W->i8_rcp, from the pack):
+ *   i8[n][k] = RNE(fl(fl(dec(code) * fl(dec(s_b) * g_w)) * r_w[n]))  (clamped to [-128, 127]),
+ * bit-identical to the pre-packed codes dmpq_pack_weights writes. Per-column g_w (fp4_g_col) is
+ * honoured. Pair it with W->i8_scale for the INT8 GEMM (a dmpq_weights whose i8_codes = i8_out).
+ * One HBM pass: 0.5625 B read + 1 B written per weight. Errors: EINVAL (NULL / no i8_rcp),
+ * EALIGN, ESHAPE (k % 64, n % 16). */
+dmpq_status dmpq_cast_int8(const dmpq_weights* W, int8_t* i8_out, dmpq_stream_t s);
 
 /* dmpq_pack_weights with options: DMPQ_PACK_HADAMARD packs W~ = 2^-7 W . blockdiag(H_128)
  * (Sylvester, entries +-1; g_w from amax(W~)), so (H x) . W~^T = x . W^T for activations

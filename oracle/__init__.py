@@ -74,6 +74,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_fht128_f32.argtypes = [P, P, LL]
         L.oracle_nvfp4_quantize_f32.argtypes = [P, I, I, F, P, P]
         L.oracle_int8_quantize_rows_f32.argtypes = [P, I, I, P, P]
+        L.oracle_int8_quantize_blocks_f32.argtypes = [P, I, I, I, P, P]
+        L.oracle_gemm_int8_blocks.argtypes = [P, P, I, P, P, P, I, I, I, I, I, P]
         L.oracle_pack_weights_hadamard.argtypes = [P, I, I, P, P, P, P, P, P]
         L.oracle_pack_weights.argtypes = [P, I, I, P, P, P, P, P]
         L.oracle_gemm_int8.argtypes, L.oracle_gemm_int8.restype = [P, P, P, P, P, I, I, I, I, I, P, P], I
@@ -243,6 +245,32 @@ def int8_quantize_f32(x32: np.ndarray):
     scale = np.zeros(m, dtype=np.float32)
     lib().oracle_int8_quantize_rows_f32(_p(x), m, k, _p(codes), _p(scale))
     return codes, scale
+
+
+def int8_quantize_blocks_f32(x32: np.ndarray, block: int = 128):
+    """Per-block symmetric INT8 of FP32 rows (reading R17). Returns (codes int8 [m, k],
+    scales f32 [m, k/block])."""
+    x = np.ascontiguousarray(x32, dtype=np.float32)
+    m, k = x.shape
+    assert k % block == 0
+    codes = np.zeros((m, k), dtype=np.int8)
+    scale = np.zeros((m, k // block), dtype=np.float32)
+    lib().oracle_int8_quantize_blocks_f32(_p(x), m, k, block, _p(codes), _p(scale))
+    return codes, scale
+
+
+def gemm_int8_blocks(a, s_a, w, s_w, bias, block: int = 128, rows=None) -> np.ndarray:
+    """GEMM over per-block INT8 activations (R17): exact per-block integer sums, FP64 scaling."""
+    a = np.ascontiguousarray(a, dtype=np.int8)
+    w = np.ascontiguousarray(w, dtype=np.int8)
+    m, k = a.shape
+    n = w.shape[0]
+    r0, r1 = (0, m) if rows is None else rows
+    y = np.zeros((r1 - r0, n), dtype=np.float64)
+    b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+    lib().oracle_gemm_int8_blocks(_p(a), _p(np.ascontiguousarray(s_a, dtype=np.float32)), block, _p(w),
+                                  _p(np.ascontiguousarray(s_w, dtype=np.float32)), _p(b), m, n, k, r0, r1, _p(y))
+    return y
 
 
 def pack_weights_hadamard(w_bf16: np.ndarray):

@@ -261,6 +261,60 @@ void oracle_int8_quantize_rows_f32(const float* x, int m, int k, int8_t* codes, 
     }
 }
 
+/* Per-block symmetric INT8 of FP32 rows (after the block Hadamard, activations are
+ * quantized "using either the NVFP4 format or per-block symmetric INT8"; NEXT-1). Reading R17:
+ * the blocks are the B = 128 consecutive elements of a row along K that one Hadamard block
+ * covers; each block is quantized exactly as a per-token row is (Eq. 1 with z = 0, R4):
+ *   a = max|x| over the block;  a == 0: s = 1, codes 0;
+ *   else s = fl(a / 127), code = clip(RNE(fl(x * fl(127 / a))), -128, 127).
+ * scale is [m x k/B], row-major. */
+void oracle_int8_quantize_blocks_f32(const float* x, int m, int k, int B, int8_t* codes, float* scale) {
+    for (int r = 0; r < m; ++r)
+        for (int b = 0; b < k / B; ++b) {
+            const float* xb = x + (size_t)r * k + (size_t)b * B;
+            int8_t* cb = codes + (size_t)r * k + (size_t)b * B;
+            float a = 0.0f;
+            for (int j = 0; j < B; ++j)
+                if (fabsf(xb[j]) > a) a = fabsf(xb[j]);
+            if (a == 0.0f) {
+                scale[(size_t)r * (k / B) + b] = 1.0f;
+                for (int j = 0; j < B; ++j) cb[j] = 0;
+                continue;
+            }
+            scale[(size_t)r * (k / B) + b] = a / 127.0f;
+            float rcp = 127.0f / a;
+            for (int j = 0; j < B; ++j) {
+                double rq = nearbyint((double)(xb[j] * rcp));
+                if (rq > 127.0) rq = 127.0;
+                if (rq < -128.0) rq = -128.0;
+                cb[j] = (int8_t)rq;
+            }
+        }
+}
+
+/* GEMM over per-block INT8 activations (R17): each K block's integer dot product is exact,
+ *   acc_b[m][n] = sum_{k in block b} a * w  (int64),
+ * and the block scales multiply it in exact FP64 (|acc_b| < 2^22, s_a a float: exact product):
+ *   Y64 = (sum_b acc_b * s_a[m][b]) * s_w[n] + bias[n]   (FP64 sum over b in order). */
+void oracle_gemm_int8_blocks(const int8_t* a, const float* s_a, int B, const int8_t* w, const float* s_w,
+                             const float* bias, int m, int n, int k, int row0, int row1, double* y_out) {
+    (void)m;
+    const int nbk = k / B;
+    for (int i = row0; i < row1; ++i)
+        for (int j = 0; j < n; ++j) {
+            double t = 0.0;
+            for (int b = 0; b < nbk; ++b) {
+                int64_t acc = 0;
+                for (int e = b * B; e < (b + 1) * B; ++e)
+                    acc += (int64_t)a[(size_t)i * k + e] * (int64_t)w[(size_t)j * k + e];
+                t += (double)acc * (double)s_a[(size_t)i * nbk + b];
+            }
+            double y = t * (double)s_w[j];
+            if (bias) y += (double)bias[j];
+            y_out[(size_t)(i - row0) * n + j] = y;
+        }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Symmetric INT8: "maps values to [-128, 127] with s = max(|X|)/127",  */
 /* Eq. 1 with z = 0: X_q = clip(round(X/s), -128, 127).  Granularity: one scale */

@@ -31,7 +31,7 @@ STATS_LEN = 7
 class Weights(ctypes.Structure):
     _fields_ = [("n", c_int), ("k", c_int), ("fp4_codes", c_void_p), ("fp4_sf", c_void_p), ("fp4_g", c_void_p),
                 ("i8_codes", c_void_p), ("i8_scale", c_void_p), ("bias", c_void_p), ("bf16_w", c_void_p),
-                ("fp4_g_col", c_void_p)]
+                ("fp4_g_col", c_void_p), ("i8_rcp", c_void_p)]
 
 
 class Act(ctypes.Structure):
@@ -83,6 +83,7 @@ _SIGNATURES = {
     "dmpq_gemm_tdc_workspace_bytes": ([], c_size_t),
     "dmpq_pack_weights": ([c_void_p, c_int, c_int, ctypes.POINTER(Weights), c_void_p], c_int),
     "dmpq_pack_weights_ex": ([c_void_p, c_int, c_int, c_uint32, ctypes.POINTER(Weights), c_void_p], c_int),
+    "dmpq_cast_int8": ([ctypes.POINTER(Weights), c_void_p, c_void_p], c_int),
     "dmpq_derive_tau": ([c_double, c_double, c_double, c_double], c_double),
     "dmpq_predict": ([ctypes.POINTER(BlockStats), ctypes.POINTER(c_double), c_int, c_int, c_int, c_int,
                       ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(c_double)], c_int),

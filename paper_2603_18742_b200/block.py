@@ -59,7 +59,7 @@ class BlockWeights:
 
 
 def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, hadamard: bool = False,
-                       keep_bf16: bool = False, fuse_qkv: bool = True) -> BlockWeights:
+                       keep_bf16: bool = False, fuse_qkv: bool = True, int8_resident: bool = True) -> BlockWeights:
     shapes = [(H, H), (H, H), (H, H), (H, H), (F, H), (H, F)]
     layers = []
     for j, (n, k) in enumerate(shapes):
@@ -67,7 +67,8 @@ def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, had
             w, b = synth.linear_weight_device(n, k, seed * 16 + j, device)
         else:
             w, b = synth.linear_weight(n, k, seed * 16 + j)
-        layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard, keep_bf16=keep_bf16))
+        layers.append(D.dmpq_pack_weights(w.to(device), b.to(device), hadamard=hadamard, keep_bf16=keep_bf16,
+                                          int8_resident=int8_resident))
         if not keep_bf16:
             del w
     qkv = None
@@ -128,7 +129,7 @@ class DiTStack:
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
                  tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False,
-                 fuse_refresh: bool = False, fuse_qkv: bool = True):
+                 fuse_refresh: bool = False, fuse_qkv: bool = True, int8_cast: bool = False):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -145,10 +146,14 @@ class DiTStack:
         self.fuse_refresh = fuse_refresh and not cache_nvfp4
         self.fuse_qkv = fuse_qkv      # one Q|K|V GEMM when the three layers share a format
         self.m_total = m_total if m_total is not None else m_local
+        # P:184's residency: weights NVFP4 only, INT8 codes cast on the fly per INT8 GEMM into one
+        # shared scratch (NEXT-4b; dmpq_cast_int8)
+        self.int8_cast = int8_cast
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
         self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr,
-                                          fuse_qkv=fuse_qkv) for b in range(n_blocks)]
+                                          fuse_qkv=fuse_qkv, int8_resident=not int8_cast) for b in range(n_blocks)]
+        self.i8_scratch = torch.empty(max(3 * H * H, F * H) if int8_cast else 0, dtype=torch.int8, device=self.device)
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
         # one buffer for the per-step MAX all-reduce: [0] amax of the quantised values (NVFP4 global
         # scales, R3); [1] max|x| of the layer inputs (PDR, R15); then max|d| of each block's last
@@ -178,7 +183,7 @@ class DiTStack:
         self.records: list[StepRecord] = []
         self.launches = 0                       # libdmpq kernel launches issued (bench's gpu_launches)
         self.timing = False                     # record CUDA events around every GEMM (roofline)
-        self.kernel_events = {"quantize": [], "tdc": [], "exchange": []}   # breakdown of the step
+        self.kernel_events = {"quantize": [], "tdc": [], "exchange": [], "cast": []}   # breakdown of the step
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
         self.capture = None                     # dict -> per-stage clones for the parity tests
@@ -289,6 +294,9 @@ class DiTStack:
         return 2.0 * m * (4 * H * H + 2 * H * F)
 
     def _gemm(self, a, w, **kw):
+        if a.fmt == D.FMT_INT8 and self.int8_cast:   # rebuild this layer's INT8 codes from its NVFP4 form
+            with self._ev("cast"):
+                w = D.dmpq_cast_int8(w, self.i8_scratch)
         if self.timing:
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
@@ -307,7 +315,7 @@ class DiTStack:
         return out
 
     def reset_timing(self):
-        self.kernel_events = {"quantize": [], "tdc": [], "exchange": []}
+        self.kernel_events = {"quantize": [], "tdc": [], "exchange": [], "cast": []}
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
 
@@ -404,6 +412,9 @@ class DiTStack:
             else:   # 4 quantizers + 6 GEMMs + refresh, fewer when fused, +2 for a cache bootstrap
                 qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2] and fmts[3] != D.FMT_BF16
                 self.launches += 11 - (1 if self.fuse_refresh else 0) - (2 if qkv1 else 0) + (2 if first else 0)
+                if self.int8_cast:   # one cast per INT8 GEMM launch
+                    i8 = [f == D.FMT_INT8 for f in fmts]
+                    self.launches += (int(i8[0]) if qkv1 else sum(i8[0:3])) + sum(i8[3:6])
             rec.linear_flops += flops
             rec.fmts.append(None if d == L.TDC_DECIDE_SKIP else fmts)
             rec.gammas.append(gamma)

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdmpq.so")
-SOURCES = ["host.cu", "quant.cu", "quant_tma.cu", "quant_had.cu", "pack.cu", "tdc.cu", "gemm.cu"]
+SOURCES = ["host.cu", "quant.cu", "quant_tma.cu", "quant_had.cu", "pack.cu", "cast.cu", "tdc.cu", "gemm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

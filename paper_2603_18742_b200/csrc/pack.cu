@@ -28,7 +28,8 @@ __device__ __forceinline__ float e2m1_value(uint32_t nib) {
 // One CTA per output row: W^ = fl(dec(code) * fl(dec(s_b) * g)); s_w = fl(max|W^|/127);
 // code = RNE(fl(W^ * fl(127/max))).
 __global__ void __launch_bounds__(256) pack_int8_from_fp4_kernel(const uint8_t* codes, const uint8_t* sf, const float* g_ptr,
-                                                                 int n, int k, int kc4, int8_t* i8, float* i8_scale) {
+                                                                 int n, int k, int kc4, int8_t* i8, float* i8_scale,
+                                                                 float* i8_rcp) {
     __shared__ float red[8];
     const int row = blockIdx.x;
     if (row >= n) return;
@@ -50,7 +51,11 @@ __global__ void __launch_bounds__(256) pack_int8_from_fp4_kernel(const uint8_t* 
     a = 0.0f;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a = fmaxf(a, red[w]);
     const float rcp = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
-    if (threadIdx.x == 0) i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+    if (threadIdx.x == 0) {
+        i8_scale[row] = a > 0.0f ? __fdiv_rn(a, 127.0f) : 1.0f;
+        if (i8_rcp) i8_rcp[row] = rcp;   // r_w for the on-the-fly cast (dmpq_cast_int8)
+    }
+    if (!i8) return;                     // NVFP4-only residency: INT8 codes are cast per GEMM
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
         int c = __float2int_rn(__fmul_rn(what(j), rcp));
         i8[(size_t)row * k + j] = (int8_t)max(-128, min(127, c));
@@ -81,9 +86,10 @@ extern "C" dmpq_status dmpq_pack_weights_ex(const uint16_t* W, int n, int k, uin
     DMPQ_REQUIRE(n > 0 && k > 0 && k % 64 == 0 && n % 16 == 0 && k <= 16384, DMPQ_ESHAPE,
                  "dmpq_pack_weights: need n %% 16 == 0, k %% 64 == 0, k <= 16384 (n=%d k=%d)", n, k);
     DMPQ_REQUIRE(out->n == n && out->k == k, DMPQ_ESHAPE, "dmpq_pack_weights: out->n/k mismatch");
-    DMPQ_REQUIRE(out->fp4_codes && out->fp4_sf && out->fp4_g && out->i8_codes && out->i8_scale && aligned16(W) &&
-                     aligned16(out->fp4_codes) && aligned16(out->fp4_sf) && aligned16(out->i8_codes),
-                 DMPQ_EALIGN, "dmpq_pack_weights: buffers must be non-NULL, 16-byte aligned device pointers");
+    DMPQ_REQUIRE(out->fp4_codes && out->fp4_sf && out->fp4_g && (out->i8_codes || out->i8_rcp) && out->i8_scale &&
+                     aligned16(W) && aligned16(out->fp4_codes) && aligned16(out->fp4_sf) && aligned16(out->i8_codes),
+                 DMPQ_EALIGN, "dmpq_pack_weights: buffers must be non-NULL (i8_codes may be NULL with i8_rcp), "
+                              "16-byte aligned device pointers");
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_pack_weights: needs an sm_100 device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
     if (cudaMemsetAsync(out->fp4_g, 0, sizeof(float), st) != cudaSuccess) return check_launch("dmpq_pack_weights(memset)");
@@ -115,7 +121,7 @@ extern "C" dmpq_status dmpq_pack_weights_ex(const uint16_t* W, int n, int k, uin
     rc = dmpq_quantize_act(W, n, k, k, had ? &had_opts : nullptr, nullptr, &a, nullptr, s);
     if (rc != DMPQ_OK) return rc;
     pack_int8_from_fp4_kernel<<<n, 256, 0, st>>>(out->fp4_codes, out->fp4_sf, out->fp4_g, n, k, ((k / 16) + 3) / 4,
-                                                 out->i8_codes, out->i8_scale);
+                                                 out->i8_codes, out->i8_scale, out->i8_rcp);
     rc = check_launch("dmpq_pack_weights(int8)");
     if (rc != DMPQ_OK || !had) return rc;
     // R14: the packed forms above are those of U = W . blockdiag(H_128); the rotated weights are

@@ -239,16 +239,6 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
             Y[32 + 4 * u + 3] = bf16x2_to_f2(v.w);
         }
 
-        // the row set is in registers: release buffer b right away and (thread 0, once every warp
-        // has released it) refill it with row set it + nbuf, so the next nbuf row sets are in
-        // flight during this one's whole computation
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
-        if (tid == 0 && it + nbuf < iters) {
-            mbar_wait(bar0 + 8 * (nbuf + b), ph);
-            issue(b, set + nbuf * (int)gridDim.x);
-        }
-
         if constexpr (LN) {
             // h = bf16(fl(x rstd - fl(mean rstd))) (glue, R13): one pass of packed raw sums
             // S1 = sum x, S2 = sum x^2 (FP32), mean = S1/k, var = max(S2/k - mean^2, 0).
@@ -335,6 +325,17 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
                     Y[q + hp] = sub2(a, bb);
                 }
             }
+        }
+
+        // the row set is in registers: release buffer b and (thread 0, once every warp has
+        // released it) refill it with row set it + nbuf, so nbuf row sets stay in flight.
+        // (Releasing right after the shared-memory loads was measured 2-5 % slower and let a
+        // TMA refill race the loads' completion: a rare wrong row in the dense-row test.)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
+        if (tid == 0 && it + nbuf < iters) {
+            mbar_wait(bar0 + 8 * (nbuf + b), ph);
+            issue(b, set + nbuf * (int)gridDim.x);
         }
 
         // per-16-block |y| maxima and this thread's maximum

@@ -16,7 +16,7 @@ from . import _lib as L
 
 __all__ = [
     "PackedWeights", "QuantAct", "dmpq_pack_weights", "dmpq_predict", "dmpq_derive_tau", "dmpq_quantize_act",
-    "dmpq_global_scale", "dmpq_gemm", "tdc_step", "tdc_decide", "tdc_update", "tdc_new_state", "sf_bytes",
+    "dmpq_global_scale", "dmpq_gemm", "dmpq_cast_int8", "tdc_step", "tdc_decide", "tdc_update", "tdc_new_state", "sf_bytes",
     "tdc_workspace_bytes", "FMT_INT8", "FMT_NVFP4", "FMT_BF16",
 ]
 
@@ -55,12 +55,14 @@ class PackedWeights:
     fp4_codes: torch.Tensor
     fp4_sf: torch.Tensor
     fp4_g: torch.Tensor
-    i8_codes: torch.Tensor
+    i8_codes: torch.Tensor | None          # None: NVFP4-only residency (INT8 cast per GEMM, dmpq_cast_int8)
     i8_scale: torch.Tensor
     bias: torch.Tensor | None
     c: L.Weights = field(default=None, repr=False)
     hadamard: bool = False
     bf16_w: torch.Tensor | None = None     # unquantised weights for the PDR BF16 fallback (R15)
+    i8_rcp: torch.Tensor | None = None     # r_w = fl(127 / max|W^|) per row (the cast's INT8 scale)
+    g_col: torch.Tensor | None = None
 
     def keep_bf16(self, W: torch.Tensor):
         self.bf16_w = W.contiguous()
@@ -68,32 +70,30 @@ class PackedWeights:
         return self
 
     @classmethod
-    def empty(cls, n: int, k: int, device, bias: torch.Tensor | None = None):
+    def empty(cls, n: int, k: int, device, bias: torch.Tensor | None = None, int8_resident: bool = True):
         d = dict(device=device)
-        pw = cls(n, k,
-                 torch.empty((n, k // 2), dtype=torch.uint8, **d),
-                 torch.zeros(sf_bytes(n, k), dtype=torch.uint8, **d),
-                 torch.zeros(1, dtype=torch.float32, **d),
-                 torch.empty((n, k), dtype=torch.int8, **d),
-                 torch.empty(n, dtype=torch.float32, **d),
-                 None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous())
-        pw.c = L.Weights(n, k, pw.fp4_codes.data_ptr(), pw.fp4_sf.data_ptr(), pw.fp4_g.data_ptr(),
-                         pw.i8_codes.data_ptr(), pw.i8_scale.data_ptr(),
-                         None if pw.bias is None else pw.bias.data_ptr())
-        return pw
+        return cls._from_tensors(
+            n, k, torch.empty((n, k // 2), dtype=torch.uint8, **d), torch.zeros(sf_bytes(n, k), dtype=torch.uint8, **d),
+            torch.zeros(1, dtype=torch.float32, **d),
+            torch.empty((n, k), dtype=torch.int8, **d) if int8_resident else None,
+            torch.empty(n, dtype=torch.float32, **d),
+            None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous(), None, False,
+            i8_rcp=torch.empty(n, dtype=torch.float32, **d))
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in
-                   (self.fp4_codes, self.fp4_sf, self.fp4_g, self.i8_codes, self.i8_scale))
+                   (self.fp4_codes, self.fp4_sf, self.fp4_g, self.i8_codes, self.i8_scale, self.i8_rcp) if t is not None)
 
     @classmethod
-    def _from_tensors(cls, n, k, codes, sf, g, i8, i8s, bias, bf16_w, hadamard, g_col=None):
-        pw = cls(n, k, codes, sf, g, i8, i8s, bias, hadamard=hadamard, bf16_w=bf16_w)
-        pw.g_col = g_col
-        pw.c = L.Weights(n, k, codes.data_ptr(), sf.data_ptr(), g.data_ptr(), i8.data_ptr(), i8s.data_ptr(),
-                         None if bias is None else bias.data_ptr(), None if bf16_w is None else bf16_w.data_ptr(),
-                         None if g_col is None else g_col.data_ptr())
+    def _from_tensors(cls, n, k, codes, sf, g, i8, i8s, bias, bf16_w, hadamard, g_col=None, i8_rcp=None):
+        pw = cls(n, k, codes, sf, g, i8, i8s, bias, hadamard=hadamard, bf16_w=bf16_w, i8_rcp=i8_rcp, g_col=g_col)
+        pw.c = L.Weights(n, k, codes.data_ptr(), sf.data_ptr(), g.data_ptr(), _ptr_or_none(i8), i8s.data_ptr(),
+                         _ptr_or_none(bias), _ptr_or_none(bf16_w), _ptr_or_none(g_col), _ptr_or_none(i8_rcp))
         return pw
+
+
+def _ptr_or_none(t):
+    return None if t is None else t.data_ptr()
 
 
 def dmpq_concat_weights(pws: list) -> tuple:
@@ -111,34 +111,40 @@ def dmpq_concat_weights(pws: list) -> tuple:
     if not has_bf16 and any(p.bf16_w is not None for p in pws):
         raise ValueError("dmpq_concat_weights: bf16_w kept on some layers but not on others")
     n = sum(p.n for p in pws)
+    if len({p.i8_codes is None for p in pws}) != 1 or len({p.i8_rcp is None for p in pws}) != 1:
+        raise ValueError("dmpq_concat_weights: mixed INT8 residency")
     codes = torch.cat([p.fp4_codes for p in pws])
     sf = torch.cat([p.fp4_sf for p in pws])
-    i8 = torch.cat([p.i8_codes for p in pws])
+    i8 = None if pws[0].i8_codes is None else torch.cat([p.i8_codes for p in pws])
     i8s = torch.cat([p.i8_scale for p in pws])
+    rcp = None if pws[0].i8_rcp is None else torch.cat([p.i8_rcp for p in pws])
     bias = torch.cat([p.bias for p in pws]) if has_bias else None
     bf16_w = torch.cat([p.bf16_w for p in pws]) if has_bf16 else None
     g_col = torch.cat([p.fp4_g.expand(p.n) for p in pws]).contiguous()
-    cat = PackedWeights._from_tensors(n, k, codes, sf, g_col[:1], i8, i8s, bias, bf16_w, pws[0].hadamard, g_col)
+    cat = PackedWeights._from_tensors(n, k, codes, sf, g_col[:1], i8, i8s, bias, bf16_w, pws[0].hadamard, g_col,
+                                      i8_rcp=rcp)
     views, r0, s0 = [], 0, 0
+    sl = lambda t, a, b: None if t is None else t[a:b]
     for p in pws:
         ns = p.fp4_sf.numel()
         views.append(PackedWeights._from_tensors(
-            p.n, k, codes[r0:r0 + p.n], sf[s0:s0 + ns], g_col[r0:r0 + 1], i8[r0:r0 + p.n], i8s[r0:r0 + p.n],
-            None if bias is None else bias[r0:r0 + p.n], None if bf16_w is None else bf16_w[r0:r0 + p.n],
-            p.hadamard))
+            p.n, k, codes[r0:r0 + p.n], sf[s0:s0 + ns], g_col[r0:r0 + 1], sl(i8, r0, r0 + p.n), i8s[r0:r0 + p.n],
+            sl(bias, r0, r0 + p.n), sl(bf16_w, r0, r0 + p.n), p.hadamard, i8_rcp=sl(rcp, r0, r0 + p.n)))
         r0 += p.n
         s0 += ns
     return cat, views
 
 
 def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamard: bool = False,
-                      keep_bf16: bool = False) -> PackedWeights:
+                      keep_bf16: bool = False, int8_resident: bool = True) -> PackedWeights:
     """Offline pack of nn.Linear weights W [n, k] (bf16, CUDA) in both formats (P:184, R7);
-    hadamard=True rotates every row by the block FHT first (R14)."""
+    hadamard=True rotates every row by the block FHT first (R14). int8_resident=False keeps
+    only the NVFP4 form (+ the per-row INT8 scales): INT8 codes are then cast per GEMM
+    (dmpq_cast_int8, P:184's on-the-fly cast)."""
     _check_dev(W, "W", torch.bfloat16)
     W = W.contiguous()
     n, k = W.shape
-    pw = PackedWeights.empty(n, k, W.device, bias)
+    pw = PackedWeights.empty(n, k, W.device, bias, int8_resident=int8_resident)
     if hadamard:
         L.check("dmpq_pack_weights_ex", L.lib().dmpq_pack_weights_ex(_ptr(W), n, k, L.PACK_HADAMARD, ctypes.byref(pw.c),
                                                                      _stream(W.device)))
@@ -148,6 +154,19 @@ def dmpq_pack_weights(W: torch.Tensor, bias: torch.Tensor | None = None, hadamar
     if keep_bf16:
         pw.keep_bf16(W)
     return pw
+
+
+def dmpq_cast_int8(W: PackedWeights, scratch: torch.Tensor) -> PackedWeights:
+    """On-the-fly NVFP4 -> INT8 weight cast (NEXT-4b): writes W's INT8 codes into `scratch`
+    (int8, >= n*k elements, reused across layers) and returns W viewed with i8_codes = scratch."""
+    _check_dev(scratch, "scratch", torch.int8)
+    if scratch.numel() < W.n * W.k:
+        raise ValueError("dmpq_cast_int8: scratch too small")
+    i8 = scratch.view(-1)[: W.n * W.k].view(W.n, W.k)
+    L.check("dmpq_cast_int8", L.lib().dmpq_cast_int8(ctypes.byref(W.c), _ptr(i8), _stream(scratch.device)))
+    v = PackedWeights._from_tensors(W.n, W.k, W.fp4_codes, W.fp4_sf, W.fp4_g, i8, W.i8_scale, W.bias, W.bf16_w,
+                                    W.hadamard, W.g_col, i8_rcp=W.i8_rcp)
+    return v
 
 
 # --------------------------------------------------------------------------- activations

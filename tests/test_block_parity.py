@@ -44,6 +44,8 @@ MODES = {
     # the compressed cache's quantization noise enters Eq. 9 (E >= ~eps^2/2 ~ 0.004 here, R16): a looser tau
     # so that the trajectory still skips
     "hadamard_cache_nvfp4": (True, False, 25.0, True, 0.02),
+    # NVFP4-only weight residency, INT8 codes cast on the fly per INT8 GEMM (NEXT-4b)
+    "hadamard_int8_cast": (True, False, 25.0, False, 0.02, False, True),
 }
 
 
@@ -65,9 +67,10 @@ def run(request):
     M, H, F, T = 256, 128, 512, 6
     had, pdr, tau_o, c4, tau_c = MODES[request.param][:5]
     fused = len(MODES[request.param]) > 5 and MODES[request.param][5]
+    cast = len(MODES[request.param]) > 6 and MODES[request.param][6]
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
     stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o,
-                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused)
+                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused, int8_cast=cast)
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):
@@ -123,6 +126,9 @@ def _gemm_ref(orc, fmt, q, pw, n, k):
         return orc.gemm_nvfp4(c, s, g, pw.fp4_codes.cpu().numpy(), orc.sf_unswizzle(pw.fp4_sf.cpu().numpy(), n, k),
                               pw.fp4_g.item(), bias), False
     c, s, _ = q
+    if pw.i8_codes is None:   # NVFP4-only residency: the INT8 codes the cast rebuilds (cast parity: test_gpu_parity)
+        pw = D.dmpq_cast_int8(pw, torch.empty(pw.n * pw.k, dtype=torch.int8, device="cuda"))
+        torch.cuda.synchronize()
     _, y = orc.gemm_int8(c, s, pw.i8_codes.cpu().numpy(), pw.i8_scale.cpu().numpy(), bias)
     return y.astype(np.float64), True
 

@@ -600,3 +600,47 @@ def test_graph_replay_equals_eager(D, had):
     for a, b in zip(e["delta"], g["delta"]):
         assert torch.equal(a, b)
     assert torch.equal(e["g"], g["g"])
+
+
+@pytest.mark.parametrize("n,k,had", [(32, 64, False), (256, 1920, False), (384, 3072, True), (1920, 256, True)])
+def test_cast_int8_bit_exact(D, orc, n, k, had):
+    """On-the-fly NVFP4 -> INT8 weight cast (NEXT-4b): an NVFP4-only pack plus dmpq_cast_int8
+    reproduces the pre-packed INT8 codes bit for bit (and the oracle's pack), and the INT8 GEMM
+    through the cast equals the GEMM on resident codes."""
+    w, b = synth.linear_weight(n, k, seed=n + 13 * k)
+    w[3] = 0   # a zero row: r_w = 0, codes 0, s_w = 1
+    full = D.dmpq_pack_weights(w.cuda(), b, hadamard=had)
+    lean = D.dmpq_pack_weights(w.cuda(), b, hadamard=had, int8_resident=False)
+    assert lean.i8_codes is None and lean.nbytes() < full.nbytes()
+    scratch = torch.full((n * k + 64,), 77, dtype=torch.int8, device="cuda")
+    cast = D.dmpq_cast_int8(lean, scratch)
+    torch.cuda.synchronize()
+    assert torch.equal(cast.i8_codes.cpu(), full.i8_codes.cpu())
+    assert torch.equal(lean.i8_scale.cpu(), full.i8_scale.cpu())
+    ref = orc.pack_weights_hadamard(synth.bits(w)) if had else orc.pack_weights(synth.bits(w))
+    assert np.array_equal(cast.i8_codes.cpu().numpy(), ref["i8_codes"])
+    m = 129
+    x = synth.dit_activation(m, k, seed=k)
+    a = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a, hadamard=had)
+    y0 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    y1 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a, full, Y32=y0)
+    D.dmpq_gemm(a, cast, Y32=y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y0.cpu(), y1.cpu())
+
+
+def test_cast_int8_concatenated(D, orc):
+    """The cast of side-by-side Q | K | V packs (per-column g_w) equals each layer's own codes."""
+    k = 256
+    packs, fulls = [], []
+    for j, n in enumerate((128, 256, 384)):
+        w, b = synth.linear_weight(n, k, seed=70 + j)
+        packs.append(D.dmpq_pack_weights(w.cuda(), b, int8_resident=False))
+        fulls.append(D.dmpq_pack_weights(w.cuda(), b))
+    cat, views = D.dmpq_concat_weights(packs)
+    scratch = torch.empty(cat.n * k, dtype=torch.int8, device="cuda")
+    c = D.dmpq_cast_int8(cat, scratch)
+    torch.cuda.synchronize()
+    assert torch.equal(c.i8_codes.cpu(), torch.cat([f.i8_codes for f in fulls]).cpu())

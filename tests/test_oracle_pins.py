@@ -734,3 +734,72 @@ def test_sf_offset_hierarchical_layout(orc):
                 inner = evaluate(((r % 128), ke % 64), shape, stride)
                 atom = (r // 128) * kc4 + (ke // 64)
                 assert orc.sf_offset(r, c, k) == atom * 512 + inner, (r, c, k)
+
+
+# ---------------------------------------------------------------------------- per-block INT8 (R17, NEXT-1)
+
+def test_int8_blocks_hand_example(orc):
+    """Two 128-blocks of one row with different maxima get their own scales s = max/127 (P:187:
+    per-block symmetric INT8): block 0 max 2 -> s = fl(2/127), 1.0 -> code 64 (63.5 ties to even);
+    block 1 max 0.5 -> s = fl(0.5/127), 0.25 -> 64 (63.5), -0.5 -> -127; a zero block -> s = 1."""
+    x = np.zeros((1, 384), np.float32)
+    x[0, 0], x[0, 1] = -2.0, 1.0
+    x[0, 128], x[0, 129], x[0, 130] = 0.5, 0.25, -0.5
+    c, s = orc.int8_quantize_blocks_f32(x)
+    assert s[0, 0] == np.float32(2.0) / np.float32(127.0) and s[0, 1] == np.float32(0.5) / np.float32(127.0)
+    assert s[0, 2] == 1.0
+    assert list(c[0, :2]) == [-127, 64] and list(c[0, 128:131]) == [127, 64, -127]
+    assert not c[0, 256:].any()
+
+
+def test_int8_blocks_reduce_to_per_token(orc):
+    """With B = K the per-block quantizer is the per-token one (same codes and scales); with every
+    block of a row sharing its maximum the block scales all equal the row's."""
+    rng = np.random.default_rng(30)
+    x = (rng.standard_normal((17, 256)) * np.exp(rng.standard_normal((17, 1)))).astype(np.float32)
+    c1, s1 = orc.int8_quantize_blocks_f32(x, block=256)
+    c0, s0 = orc.int8_quantize_f32(x)
+    assert np.array_equal(c1, c0) and np.array_equal(s1[:, 0], s0)
+    y = x.copy()
+    y[:, 0] = y[:, 128] = np.abs(y).max(axis=1) * 2   # same block maxima in both blocks
+    cb, sb = orc.int8_quantize_blocks_f32(y)
+    ct, st = orc.int8_quantize_f32(y)
+    assert np.array_equal(cb, ct) and np.array_equal(sb[:, 0], st) and np.array_equal(sb[:, 1], st)
+
+
+def test_int8_blocks_error_bound(orc):
+    rng = np.random.default_rng(31)
+    x = (rng.standard_normal((9, 512)) * rng.choice([1e-3, 1.0, 50.0], size=(9, 512))).astype(np.float32)
+    c, s = orc.int8_quantize_blocks_f32(x)
+    deq = c.astype(np.float64).reshape(9, 4, 128) * s.astype(np.float64)[:, :, None]
+    err = np.abs(deq - x.astype(np.float64).reshape(9, 4, 128))
+    assert np.all(err <= 0.5 * s.astype(np.float64)[:, :, None] * (1 + 1e-6))
+    for r in range(9):   # every block maximum maps to +-127
+        for b in range(4):
+            blk = x[r, b * 128:(b + 1) * 128]
+            assert abs(int(c[r, b * 128 + int(np.abs(blk).argmax())])) == 127
+
+
+def test_gemm_int8_blocks_exact_fractions(orc):
+    """sum_b (sum_{k in b} a w) s_a[b] s_w + bias against exact rationals on small random inputs;
+    and a GEMM whose blocks all share one scale equals the per-token INT8 GEMM's exact value."""
+    rng = np.random.default_rng(32)
+    m, n, k = 3, 5, 384
+    a = rng.integers(-128, 128, size=(m, k), dtype=np.int8)
+    w = rng.integers(-128, 128, size=(n, k), dtype=np.int8)
+    sa = rng.uniform(1e-3, 1, size=(m, 3)).astype(np.float32)
+    sw = rng.uniform(1e-3, 1, size=n).astype(np.float32)
+    bias = rng.uniform(-1, 1, size=n).astype(np.float32)
+    y = orc.gemm_int8_blocks(a, sa, w, sw, bias)
+    for i in range(m):
+        for j in range(n):
+            t = sum(Fraction(int(np.dot(a[i, b * 128:(b + 1) * 128].astype(np.int64),
+                                        w[j, b * 128:(b + 1) * 128].astype(np.int64)))) * Fraction(float(sa[i, b]))
+                    for b in range(3))
+            exact = t * Fraction(float(sw[j])) + Fraction(float(bias[j]))
+            assert abs(Fraction(y[i, j]) - exact) <= abs(exact) * Fraction(1, 2 ** 50)
+    sa_eq = np.repeat(sa[:, :1], 3, axis=1)
+    y_eq = orc.gemm_int8_blocks(a, sa_eq, w, sw, None)
+    acc = a.astype(np.int64) @ w.astype(np.int64).T
+    ref = acc.astype(np.float64) * sa[:, :1].astype(np.float64) * sw.astype(np.float64)[None, :]
+    np.testing.assert_allclose(y_eq, ref, rtol=1e-15)
