@@ -457,8 +457,8 @@ def run_ours(args):
     peaks, peak_kind = load_peaks()
 
     model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
-                     pdr=args.pdr, m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh,
-                     int8_cast=args.int8_cast)
+                     pdr={None: False, "delayed": True, "current": "current"}[args.pdr], m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh,
+                     int8_cast=args.int8_cast, int8_block=args.int8_block)
     # block-0 input trajectory basis: ONE seeded global [M x H] input, of which this rank takes its
     # contiguous row shard -- every world size solves the same problem (same mix, same decisions)
     A, B = synth.trajectory_basis(M, H, seed=1000 + args.seed, device=dev)
@@ -680,7 +680,8 @@ def run_ours(args):
                    "device_map": os.environ.get("DMPQ_DEVICE_MAP", "one GPU per rank"),
                    "input": "one seeded global input; each rank takes its contiguous row shard", "l2": "inputs larger than L2 (multi-GB working set per step)",
                    "cuda_graphs": not args.no_graphs, "tdc_refresh": "fused in the FFN2 GEMM epilogue" if model.fuse_refresh else "own kernel",
-                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr, "int8_weight_cast": args.int8_cast,
+                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr or False, "int8_weight_cast": args.int8_cast,
+                   "int8_granularity": "per 128-block (R17)" if args.int8_block else "per token (R2)",
                    "delta_cache": {"format": "nvfp4" if args.cache_nvfp4 else "bf16",
                                    "bytes_per_rank": sum(d.nbytes() if args.cache_nvfp4 else d.numel() * 2
                                                          for d in model.delta)},
@@ -738,17 +739,23 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel eagerly (no CUDA graphs)")
     ap.add_argument("--no-hadamard", action="store_true", help="disable the online block-Hadamard smoothing (P:187)")
-    ap.add_argument("--pdr", action="store_true", help="enable the Purified Cache Refresh outlier gate (P:241, "
-                    "NEXT-3; off by default: the north_star path is DMPQ + TDC)")
+    ap.add_argument("--pdr", nargs="?", const="delayed", default=None, choices=["delayed", "current"],
+                    help="enable the Purified Cache Refresh outlier gate (P:241, NEXT-3; off by default: the north_star "
+                    "path is DMPQ + TDC): 'delayed' (R15, all-rank R of the last computed step, host decision) or "
+                    "'current' (R18, this step's input, decided on the device, both GEMM kinds predicated)")
     ap.add_argument("--rank-share", type=int, default=0, help="development: time one rank's token share of an "
                     "N-GPU run on this GPU (host-overhead study; not a bench line)")
     ap.add_argument("--bounds", action="store_true", help="also time all-NVFP4 and all-INT8 steps without skips "
                     "(SURVEY 8(d) bounds)")
     ap.add_argument("--fused-refresh", action="store_true", help="run the TDC refresh in the FFN2 GEMM epilogue "
                     "instead of its own kernel (SURVEY NEXT-2; measured slower, DESIGN.md 5.7c)")
+    ap.add_argument("--int8-block", action="store_true", help="per-block symmetric INT8 activations over the 128-element "
+                    "Hadamard blocks (P:187, R17, NEXT-1) instead of per-token INT8")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
-    ap.add_argument("--int8-cast", action="store_true", help="NVFP4-only weight residency, INT8 codes cast on the fly "
-                    "per INT8 GEMM (P:184, NEXT-4b)")
+    ap.add_argument("--no-int8-cast", dest="int8_cast", action="store_false",
+                    help="keep both weight forms resident (default: NVFP4-only residency, INT8 codes cast on the fly "
+                    "per INT8 GEMM into an L2-resident scratch, P:184, NEXT-4b: 3.5x less weight memory and measured "
+                    "faster, DESIGN.md 5.7b)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs --warmup >= 3", file=sys.stderr)

@@ -109,7 +109,10 @@ typedef struct {
     void* codes;           /* NVFP4: uint8 [m x k/2]; INT8: int8 [m x k]; BF16: the bf16 activation [m x k] (row-major, dense) */
     uint8_t* sf;           /* NVFP4: dmpq_sf_bytes(m, k) block scales; INT8: unused */
     const float* g;        /* NVFP4: device FP32 per-tensor scale g_a (input of the quantizer) */
-    float* row_scale;      /* INT8: [m] per-token scale s = amax_row/127 (R2) */
+    float* row_scale;      /* INT8: [m] per-token scale s = amax_row/127 (R2), or with scale_block == 128:
+                              [m x k/128] per-block scales s = amax_block/127, row-major (R17) */
+    int scale_block;       /* INT8: 0 = per-token (R2); 128 = per-block symmetric INT8 over the 128-element
+                              Hadamard blocks (R17; needs DMPQ_QF_HADAMARD in the quantizer) */
 } dmpq_act;
 
 /* ========================================================================== */
@@ -187,6 +190,12 @@ dmpq_status dmpq_predict(const dmpq_block_stats* st, const double* tau_gamma, in
  * ratio may be NULL (no outlier gate). */
 void dmpq_purify(const double* ratio, int n_layers, int prev_skipped, double tau_outlier, uint8_t* fmt_inout);
 
+/* Outlier ratio of the PDR gate ("R_outlier = max|X| / mean|X|"), host-pure:
+ * R = max_abs / (sum_abs / count) in FP64; an all-zero input (sum_abs == 0) has R = 1 (no
+ * outliers, never BF16). The delayed gate (R15) evaluates it on the all-rank statistics of the
+ * block's last computed step. */
+double dmpq_outlier_ratio(double max_abs, double sum_abs, double count);
+
 /* ========================================================================== */
 /* 3. dmpq_quantize_act                                                       */
 /* ========================================================================== */
@@ -222,7 +231,8 @@ typedef struct {
  *  (atomic; the caller zeroes it once per step). With DMPQ_QF_LAYERNORM the
  *  quantised (and amax'd) values are the bf16-rounded normalised rows.
  *  With DMPQ_QF_HADAMARD the values quantised (and amax'd) are the FP32 FHT outputs
- *  y = H_128 x / sqrt(128) per 128-block, butterflies h = 1..64 in FP32 (R14).
+ *  y = H_128 x per 128-block (Sylvester, entries +-1, no normalization on the activation side:
+ *  the 2^-7 rides on the Hadamard-packed weights), butterflies h = 1..64 in FP32 (R14).
  *  Shapes: k % 64 == 0 (k % 128 == 0 with DMPQ_QF_HADAMARD), 0 < k <= 16384, m >= 0. */
 dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
                               dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s);
@@ -230,6 +240,16 @@ dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dm
 /* FP64 totals of per-row sums for the PDR outlier ratio (R15): out[s] = sum_r
  * row_sums[s*m + r] for s < segments, fixed order (deterministic). */
 dmpq_status dmpq_outlier_reduce(const float* row_sums, int m, int segments, double* out, dmpq_stream_t s);
+
+/* The paper-literal (current-input) PDR gate on the device (reading R18): from the
+ * per-row sums |x| (row_abs_sum [m], FP32, as dmpq_quantize_act writes them) and max|x|
+ * (*amax_in) of THIS step's layer input, one CTA computes
+ *   sum = dmpq_outlier_reduce's FP64 total (same order),  R = dmpq_outlier_ratio(max, sum, count),
+ *   *flag_out = R > tau_outlier ? 1 : 0,  *sum_out = sum (if non-NULL),
+ * so the GEMMs of that input can be chosen on the device (dmpq_epilogue.run_if) with no host
+ * round trip. count = the number of elements the statistics cover (m * k). */
+dmpq_status dmpq_outlier_gate(const float* row_abs_sum, int m, const float* amax_in, double count, double tau_outlier,
+                              double* sum_out, int* flag_out, dmpq_stream_t s);
 
 /* Device-side global scale for the next NVFP4 quantization (R3):
  * g_out[i] = max(fl(amax[i] / div), FLT_MIN) for i < count (div = 2688 for a
@@ -263,6 +283,12 @@ typedef struct {
     uint16_t* tdc_delta;
     double* tdc_stats;
     void* tdc_workspace;
+    /* Device-predicated launch (R18): when run_if != NULL the kernel does nothing unless
+     * *run_if == run_if_value (read on the device at kernel start), so a BF16 and a quantized
+     * GEMM of one layer can both be enqueued (or captured in one CUDA graph) and the device-side
+     * outlier gate (dmpq_outlier_gate) picks the one that runs. */
+    const int* run_if;
+    int run_if_value;
 } dmpq_epilogue;
 
 /* Workspace bytes of the fused TDC refresh (DMPQ_EP_TDC_REFRESH) on the current device. */

@@ -36,7 +36,7 @@ class Weights(ctypes.Structure):
 
 class Act(ctypes.Structure):
     _fields_ = [("fmt", c_int), ("m", c_int), ("k", c_int), ("codes", c_void_p), ("sf", c_void_p), ("g", c_void_p),
-                ("row_scale", c_void_p)]
+                ("row_scale", c_void_p), ("scale_block", c_int)]
 
 
 class QuantOpts(ctypes.Structure):
@@ -46,7 +46,8 @@ class QuantOpts(ctypes.Structure):
 
 class Epilogue(ctypes.Structure):
     _fields_ = [("flags", c_uint32), ("gate", c_void_p), ("residual", c_void_p), ("ldr", c_int),
-                ("tdc_x_in", c_void_p), ("tdc_delta", c_void_p), ("tdc_stats", c_void_p), ("tdc_workspace", c_void_p)]
+                ("tdc_x_in", c_void_p), ("tdc_delta", c_void_p), ("tdc_stats", c_void_p), ("tdc_workspace", c_void_p),
+                ("run_if", c_void_p), ("run_if_value", c_int)]
 
 
 class BlockStats(ctypes.Structure):
@@ -89,6 +90,8 @@ _SIGNATURES = {
                       ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(c_double)], c_int),
     "dmpq_quantize_act": ([c_void_p, c_int, c_int, c_int, ctypes.POINTER(QuantOpts), ctypes.POINTER(Act),
                            ctypes.POINTER(Act), c_void_p, c_void_p], c_int),
+    "dmpq_outlier_gate": ([c_void_p, c_int, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p], c_int),
+    "dmpq_outlier_ratio": ([c_double, c_double, c_double], c_double),
     "dmpq_global_scale": ([c_void_p, c_float, c_void_p, c_int, c_void_p], c_int),
     "dmpq_outlier_reduce": ([c_void_p, c_int, c_int, c_void_p, c_void_p], c_int),
     "dmpq_purify": ([ctypes.POINTER(c_double), c_int, c_int, c_double, ctypes.POINTER(ctypes.c_uint8)], None),

@@ -84,7 +84,7 @@ def make_block_weights(H: int, F: int, seed: int, device, gate_scale: float, had
 class Workspace:
     """Activation buffers for one block evaluation of m rows (reused by every block)."""
 
-    def __init__(self, m: int, H: int, F: int, device, g_table: torch.Tensor):
+    def __init__(self, m: int, H: int, F: int, device, g_table: torch.Tensor, int8_block: int = 0):
         self.m, self.H, self.F = m, H, F
         e = dict(dtype=torch.bfloat16, device=device)
         self.qkv = torch.empty(m, 3 * H, **e)    # Q | K | V outputs (Q, K unused by the stand-in attention)
@@ -96,7 +96,7 @@ class Workspace:
         self.g_table = g_table                     # [n_blocks, 4] fp32 NVFP4 global scales
         self.acts = {}
         for slot, k in enumerate((H, H, H, F)):
-            self.acts[(slot, D.FMT_INT8)] = D.QuantAct.empty(D.FMT_INT8, m, k, device)
+            self.acts[(slot, D.FMT_INT8)] = D.QuantAct.empty(D.FMT_INT8, m, k, device, scale_block=int8_block)
             self.acts[(slot, D.FMT_NVFP4)] = D.QuantAct.empty(D.FMT_NVFP4, m, k, device, g=g_table[0, slot:slot + 1])
         self.tdc_ws = torch.zeros(D.tdc_workspace_bytes(m, H), dtype=torch.uint8, device=device)
         # fused refresh in the FFN2 epilogue (zero-filled once; the kernel resets its counter)
@@ -129,7 +129,7 @@ class DiTStack:
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
                  tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False,
-                 fuse_refresh: bool = False, fuse_qkv: bool = True, int8_cast: bool = False):
+                 fuse_refresh: bool = False, fuse_qkv: bool = True, int8_cast: bool = False, int8_block: bool = False):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -138,7 +138,11 @@ class DiTStack:
         self.force_fmt = force_fmt
         self.group = group
         self.hadamard = hadamard      # online block-Hadamard smoothing (R14)
-        self.pdr = pdr                # Purified Cache Refresh outlier gate (R15)
+        # Purified Cache Refresh outlier gate: True / "delayed" = R from the block's last
+        # computed step over all ranks, decided on the host (R15); "current" = R of this step's
+        # layer input, decided on the device, both GEMM kinds enqueued and predicated (R18)
+        self.pdr = bool(pdr)
+        self.pdr_current = pdr == "current"
         self.tau_outlier = tau_outlier
         self.cache_nvfp4 = cache_nvfp4  # NVFP4-compressed delta cache (R16)
         # bf16 cache, optional: the TDC refresh runs in the FFN2 GEMM's epilogue (
@@ -149,6 +153,11 @@ class DiTStack:
         # P:184's residency: weights NVFP4 only, INT8 codes cast on the fly per INT8 GEMM into one
         # shared scratch (NEXT-4b; dmpq_cast_int8)
         self.int8_cast = int8_cast
+        # per-block symmetric INT8 activations over the 128-element Hadamard blocks (R17,
+        # NEXT-1) instead of per-token INT8 (R2); needs the Hadamard option
+        if int8_block and not hadamard:
+            raise ValueError("per-block INT8 (R17) is defined on the Hadamard blocks: needs hadamard=True")
+        self.int8_block = int8_block
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
         self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr,
@@ -163,7 +172,7 @@ class DiTStack:
         self.delta_amax = self.amax_all[2 * n_blocks * N_SLOTS:]
         self.g_delta = torch.zeros(n_blocks, dtype=torch.float32, device=self.device)
         self.row_abs = torch.zeros(n_blocks * N_SLOTS, m_local, dtype=torch.float32, device=self.device)
-        self.ws = Workspace(m_local, H, F, self.device, self.g_table)
+        self.ws = Workspace(m_local, H, F, self.device, self.g_table, int8_block=128 if int8_block else 0)
         if cache_nvfp4:
             self.delta = [D.DeltaCacheNvfp4(m_local, H, self.device) for _ in range(n_blocks)]
         else:
@@ -194,6 +203,7 @@ class DiTStack:
         self.graph_pool = None
         self.x_in0 = torch.empty(m_local, H, dtype=torch.bfloat16, device=self.device)
         self.pdr_sums = torch.zeros(n_blocks * N_SLOTS, dtype=torch.float64, device=self.device)
+        self.pdr_flags = torch.zeros(n_blocks, N_SLOTS, dtype=torch.int32, device=self.device)   # R18 device gate
 
     def _cap(self, key, t):
         if self.capture is not None:
@@ -237,7 +247,7 @@ class DiTStack:
 
     def _quant_impl(self, b, slot, src, fmts_needed, layernorm, h_buf):
         ws = self.ws
-        want_h = layernorm and (D.FMT_BF16 in fmts_needed or self.capture is not None)
+        want_h = layernorm and (D.FMT_BF16 in fmts_needed or self.capture is not None or self.pdr_current)
         a8 = ws.act(slot, D.FMT_INT8, b) if D.FMT_INT8 in fmts_needed else None
         a4 = ws.act(slot, D.FMT_NVFP4, b) if D.FMT_NVFP4 in fmts_needed else None
         D.dmpq_quantize_act(src, out_i8=a8, out_fp4=a4, amax_out=self.amax[0, b, slot:slot + 1], layernorm=layernorm,
@@ -249,7 +259,53 @@ class DiTStack:
             out[D.FMT_BF16] = D.QuantAct.bf16(h_buf if layernorm else src)
         return out
 
+    def _gate(self, b, slot, k):
+        """R18: this step's outlier ratio of the slot's input on the device -> pdr_flags[b, slot]."""
+        with self._ev("quantize"):
+            D.dmpq_outlier_gate(self.row_abs[b * N_SLOTS + slot], self.amax[1, b, slot:slot + 1], float(self.m * k),
+                                self.tau_outlier, self.pdr_flags[b, slot:slot + 1])
+
+    def _gemm_gated(self, b, slot, q, fmt, w, **kw):
+        """Both GEMM kinds of one layer, predicated on the device gate (R18): the quantized one
+        runs iff pdr_flags[b, slot] == 0, the BF16 one iff it is 1."""
+        flag = self.pdr_flags[b, slot:slot + 1]
+        self._gemm(q[fmt], w, run_if=flag, run_if_value=0, **kw)
+        self._gemm(q[D.FMT_BF16], w, run_if=flag, run_if_value=1, **kw)
+
+    def _compute_block_current(self, b: int, x_in: torch.Tensor, x_out: torch.Tensor, fmts) -> float:
+        """One block with the current-input PDR gate (R18): each layer input's quantizer
+        also writes the statistics (and the dense bf16 input), a one-CTA kernel takes the BF16 /
+        quantized decision on the device, and both GEMM kinds are enqueued, predicated on it."""
+        W, ws, H, F = self.blocks[b], self.ws, self.H, self.F
+        q0 = self._quant(b, 0, x_in, set(fmts[0:3]) | {D.FMT_BF16}, layernorm=True, h_buf=ws.h1)
+        self._gate(b, 0, H)
+        if self.capture is not None:
+            self._cap("x_in", x_in); self._cap("h1", ws.h1)
+            self._cap_act("a0_i8", q0[D.FMT_INT8]); self._cap_act("a0_f4", q0[D.FMT_NVFP4])
+        for j, out in ((0, ws.qk), (1, ws.qkv[:, H:2 * H]), (2, ws.v_dense)):   # V dense: O may run BF16
+            self._gemm_gated(b, 0, q0, fmts[j], W.layers[j], Y=out)
+            self._cap(f"y{j}", out)
+        q1 = self._quant(b, 1, ws.v_dense, {fmts[3], D.FMT_BF16})
+        self._gate(b, 1, H)
+        self._cap_act("a1", q1[fmts[3]])
+        self._gemm_gated(b, 1, q1, fmts[3], W.layers[3], Y=ws.x_mid, residual=x_in, gate=W.g1)
+        self._cap("x_mid", ws.x_mid)
+        q2 = self._quant(b, 2, ws.x_mid, {fmts[4], D.FMT_BF16}, layernorm=True, h_buf=ws.h2)
+        self._gate(b, 2, H)
+        self._cap("h2", ws.h2)
+        self._cap_act("a2", q2[fmts[4]])
+        self._gemm_gated(b, 2, q2, fmts[4], W.layers[4], Y=ws.f, gelu=True)
+        self._cap("f", ws.f)
+        q3 = self._quant(b, 3, ws.f, {fmts[5], D.FMT_BF16})
+        self._gate(b, 3, F)
+        self._cap_act("a3", q3[fmts[5]])
+        self._gemm_gated(b, 3, q3, fmts[5], W.layers[5], Y=x_out, residual=ws.x_mid, gate=W.g2)
+        self._cap("x_out", x_out)
+        return 2.0 * self.m * (4 * H * H + 2 * H * F)
+
     def _compute_block(self, b: int, x_in: torch.Tensor, x_out: torch.Tensor, fmts, refresh_stats=None) -> float:
+        if self.pdr_current:
+            return self._compute_block_current(b, x_in, x_out, fmts)
         W, ws, H, F, m = self.blocks[b], self.ws, self.H, self.F, self.m
         cap = self.capture is not None
         # attention input: LN fused into the quantizer, one pass for every format Q/K/V need
@@ -383,7 +439,9 @@ class DiTStack:
                     fmts = [self.force_fmt] * 6
                 else:
                     fmts, gamma, _ = D.dmpq_predict(self.prev_stats[b], self.tau, t, self.prev_skipped[b])
-                    if self.pdr and self.ratio[b] is not None:
+                    if self.pdr_current:   # post-skip INT8 now; the BF16 choice is taken on the device (R18)
+                        fmts = D.dmpq_purify(fmts, None, self.prev_skipped[b], self.tau_outlier)
+                    elif self.pdr and self.ratio[b] is not None:
                         fmts = D.dmpq_purify(fmts, [self.ratio[b][s] for s in SLOT_OF_LAYER], self.prev_skipped[b],
                                              self.tau_outlier)
             first = self.cache_nvfp4 and d != L.TDC_DECIDE_SKIP and self.tdc[b].n_computed == 0
@@ -410,8 +468,10 @@ class DiTStack:
             if d == L.TDC_DECIDE_SKIP:
                 self.launches += 1
             else:   # 4 quantizers + 6 GEMMs + refresh, fewer when fused, +2 for a cache bootstrap
-                qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2] and fmts[3] != D.FMT_BF16
+                qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2] and fmts[3] != D.FMT_BF16 and not self.pdr_current
                 self.launches += 11 - (1 if self.fuse_refresh else 0) - (2 if qkv1 else 0) + (2 if first else 0)
+                if self.pdr_current:   # + 4 device gates + the predicated-off GEMM of every layer
+                    self.launches += 4 + 6
                 if self.int8_cast:   # one cast per INT8 GEMM launch
                     i8 = [f == D.FMT_INT8 for f in fmts]
                     self.launches += (int(i8[0]) if qkv1 else sum(i8[0:3])) + sum(i8[3:6])
@@ -445,6 +505,12 @@ class DiTStack:
         stats = combine_host(self.slots).reshape(self.nb, N_STATS)
         if self.pdr:
             amax_in = self.amax[1].cpu().numpy().astype(np.float64)
+        if self.pdr_current:   # the device gate's decisions of this step -> the step record
+            flags = self.pdr_flags.cpu().numpy()
+            rec = self.records[-1]
+            for b in range(self.nb):
+                if rec.fmts[b] is not None:
+                    rec.fmts[b] = [D.FMT_BF16 if flags[b, SLOT_OF_LAYER[j]] else f for j, f in enumerate(rec.fmts[b])]
         rec = self.records[-1]
         for b in range(self.nb):
             d = rec.decisions[b]
@@ -459,8 +525,8 @@ class DiTStack:
                 self.prev_skipped[b] = False
                 if self.pdr:   # R = max|x| / mean|x| of each layer input over all tokens (R15)
                     ks = (self.H, self.H, self.H, self.F)
-                    self.ratio[b] = [float(amax_in[b, s]) / (stats[b][L.STATS_LEN + s] / (self.m_total * ks[s]))
-                                     if stats[b][L.STATS_LEN + s] > 0 else 1.0 for s in range(N_SLOTS)]
+                    self.ratio[b] = [D.dmpq_outlier_ratio(amax_in[b, s], stats[b][L.STATS_LEN + s], self.m_total * ks[s])
+                                     for s in range(N_SLOTS)]
         return stats
 
     def mix(self, records=None):

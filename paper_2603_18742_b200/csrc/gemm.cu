@@ -60,6 +60,9 @@ struct GemmParams {
     double* tdc_stats;
     double* tdc_partials;      // [gridDim.x * EPI_WARPS][7]
     unsigned int* tdc_counter;
+    // device-predicated launch (R18): run only when *run_if == run_if_value
+    const int* run_if;
+    int run_if_value;
 };
 
 constexpr int BM = 128;
@@ -80,6 +83,22 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8
 #define DMPQ_EPI_WARPS 8
 #endif
 constexpr int EPI_WARPS = DMPQ_EPI_WARPS;   // epilogue warps per CTA (2 per TMEM lane quarter, column-interleaved)
+#ifndef DMPQ_GEMM_PREFETCH
+#define DMPQ_GEMM_PREFETCH 0   // L2 prefetch of the next tile's A / B rows at the start of each tile (measured 25-30 % slower)
+#endif
+#ifndef DMPQ_GEMM_RASTER
+#define DMPQ_GEMM_RASTER 0     // 0: pair c takes tiles c, c + P, ... (n-fastest); 1: a contiguous run of tiles per pair
+#endif
+// the tiles of CTA pair `cid` of `ncl`: for (t = t0; t < t1; t += step)
+__device__ __forceinline__ void tile_span(int cid, int ncl, int num_tiles, int& t0, int& t1, int& step) {
+    if (DMPQ_GEMM_RASTER) {
+        t0 = (int)(((long long)cid * num_tiles) / ncl);
+        t1 = (int)(((long long)(cid + 1) * num_tiles) / ncl);
+        step = 1;
+    } else {
+        t0 = cid; t1 = num_tiles; step = ncl;
+    }
+}
 
 template <int KIND, int BN, int STAGES>   // KIND: 0 INT8, 1 NVFP4, 2 BF16
 struct PairLayout {
@@ -113,6 +132,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     using L = PairLayout<KIND, BN, STAGES>;
     constexpr bool FP4 = KIND == 1;
     constexpr bool I8 = KIND == 0;
+    // device-predicated launch: every CTA of the grid reads the same flag, so whole clusters exit
+    // together before any barrier, TMEM allocation or TMA is touched
+    if (p.run_if && *p.run_if != p.run_if_value) return;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -158,15 +180,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     const uint32_t tmem_base = *tmem_holder;
     const int num_tiles = p.num_m_tiles * p.num_n_tiles;   // pair tiles (256 rows each)
     const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+    int ts0, ts1, tstep;
+    tile_span(cid, ncl, num_tiles, ts0, ts1, tstep);
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs; whole warp, one elected issuer) =====================
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        for (int tile = ts0; tile < ts1; tile += tstep) {
             const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int m0 = mt * 256 + (int)rank * BM;
             const int nb0 = nt * BN + (int)rank * (BN / 2);
+            if (DMPQ_GEMM_PREFETCH && tile + tstep < ts1) {
+                // the next tile's A and B rows -> L2 a whole tile ahead: at short K the stage ring
+                // (~1 us deep) cannot hide a DRAM miss at every tile start (ncu: the MMA warp waited
+                // on the full barrier ~35 % of its time at K = 3072)
+                const int mt2 = (tile + tstep) / p.num_n_tiles, nt2 = (tile + tstep) % p.num_n_tiles;
+                const int m2 = mt2 * 256 + (int)rank * BM, n2 = nt2 * BN + (int)rank * (BN / 2);
+                if (elect_one()) {
+                    for (int kb = 0; kb < p.num_kb; ++kb) {
+                        tma_prefetch_2d(&tmA, kb * BK_BYTES, m2);
+                        tma_prefetch_2d(&tmB, kb * BK_BYTES, n2);
+                    }
+                }
+                __syncwarp();
+            }
             for (int kb = 0; kb < p.num_kb; ++kb) {
                 mbar_wait(bar_empty + 8 * stage, phase ^ 1);
                 if (elect_one()) {
@@ -199,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             if constexpr (FP4) idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
             else if constexpr (I8) idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
             else idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);  // F32 acc, BF16 x BF16
-            for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+            for (int tile = ts0; tile < ts1; tile += tstep, ++local) {
                 const int nt = tile % p.num_n_tiles;
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
@@ -282,7 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         const bool has_tdc = TDC && (p.flags & DMPQ_EP_TDC_REFRESH) != 0;
         // fused TDC refresh statistics of this warp's rows / chunks over all its tiles (fixed order)
         double tacc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++local) {
+        for (int tile = ts0; tile < ts1; tile += tstep, ++local) {
             const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -557,6 +595,226 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     if (warp == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
 }
 
+// ============================================================================
+// Per-block INT8 GEMM ("per-block symmetric INT8"; R17, NEXT-1): A carries one
+// scale per 128-element K block of each row, so K blocks cannot share one integer accumulator.
+// The kind::i8 MMAs of one 128-K block accumulate exactly into a TMEM partial (two partials
+// ping-pong), and the epilogue warps promote every partial into FP32 registers,
+//   t += float(P_b) * s_a[row][b]    (float(P_b) exact: |P_b| <= 128 * 127 * 128 < 2^24),
+// then y = fma(t, s_w[n], bias[n]) (+ GELU / gated-residual glue). One promotion (a conversion
+// and an FMA) per output element per 128-K block costs about as many issue slots as the MMA
+// takes cycles, so this kernel is epilogue-bound by construction.
+// CTA pair, 256 x 192 tiles, 12 epilogue warps (3 per TMEM lane quarter, 64 columns each).
+// ============================================================================
+constexpr int I8B_BN = 192;
+constexpr int I8B_EPI_WARPS = 12;
+constexpr int I8B_STAGES = 5;
+
+struct I8BLayout {
+    static constexpr int A_BYTES = BM * BK_BYTES;                   // 16 KB
+    static constexpr int B_BYTES = (I8B_BN / 2) * BK_BYTES;         // 12 KB
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int PAIR_TX = 2 * STAGE_BYTES;
+    static constexpr int BAR_OFFSET = I8B_STAGES * STAGE_BYTES;
+    static constexpr int TOTAL = BAR_OFFSET + 256 + 1024;
+    static_assert(STAGE_BYTES % 1024 == 0, "stage alignment");
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * I8B_EPI_WARPS, 1)
+    dmpq_gemm_i8b_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const GemmParams p) {
+    using L = I8BLayout;
+    constexpr int BN = I8B_BN;
+    if (p.run_if && *p.run_if != p.run_if_value) return;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar_full = sbase + L::BAR_OFFSET;
+    const uint32_t bar_empty = bar_full + I8B_STAGES * 8;
+    const uint32_t bar_pfull = bar_empty + I8B_STAGES * 8;
+    const uint32_t bar_pempty = bar_pfull + 2 * 8;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFFSET + 2 * I8B_STAGES * 8 + 4 * 8);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+        for (int s = 0; s < I8B_STAGES; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(bar_pfull + 8 * a, 1);
+            mbar_init(bar_pempty + 8 * a, 2 * I8B_EPI_WARPS);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_pair(smem_u32(tmem_holder), 512);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+    const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+    int ts0, ts1, tstep;
+    tile_span(cid, ncl, num_tiles, ts0, ts1, tstep);
+
+    if (warp == 0) {
+        // ===== TMA producer (as the INT8 pair kernel)
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = ts0; tile < ts1; tile += tstep) {
+            const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;
+            const int m0 = mt * 256 + (int)rank * BM;
+            const int nb0 = nt * BN + (int)rank * (BN / 2);
+            for (int kb = 0; kb < p.num_kb; ++kb) {
+                mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                if (elect_one()) {
+                    const uint32_t full_l = leader_addr(bar_full + 8 * stage);
+                    if (rank == 0) mbar_arrive_expect_tx(bar_full + 8 * stage, L::PAIR_TX);
+                    const uint32_t sA = sbase + stage * L::STAGE_BYTES;
+                    tma_load_2d_pair(sA, &tmA, kb * BK_BYTES, m0, full_l);
+                    tma_load_2d_pair(sA + L::A_BYTES, &tmB, kb * BK_BYTES, nb0, full_l);
+                }
+                __syncwarp();
+                if (++stage == I8B_STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (leader CTA): one TMEM partial per 128-K block, two partials ping-pong
+        if (rank == 0) {
+            int stage = 0;
+            uint32_t phase = 0, g = 0;
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            for (int tile = ts0; tile < ts1; tile += tstep) {
+                for (int kb = 0; kb < p.num_kb; ++kb, ++g) {
+                    const uint32_t pb = g & 1u, pph = (g >> 1) & 1u;
+                    mbar_wait(bar_pempty + 8 * pb, pph ^ 1);     // the epilogue has read this partial's last use
+                    tc_fence_after();
+                    mbar_wait(bar_full + 8 * stage, phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t sA = sbase + stage * L::STAGE_BYTES;
+                        const uint64_t adesc = sdesc_k_sw128(sA), bdesc = sdesc_k_sw128(sA + L::A_BYTES);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            mma_i8_pair(tmem_base + pb * BN, adesc + 2 * j, bdesc + 2 * j, idesc, j ? 1u : 0u);
+                        tc_commit_pair_mc(bar_empty + 8 * stage, 0x3);
+                        tc_commit_pair_mc(bar_pfull + 8 * pb, 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == I8B_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: promotion of every K-block partial, then the output of the tile
+        const int q = warp & 3, ew = warp - 4, csub = ew >> 2;   // lane quarter, 64-column slice
+        const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0, has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
+        const bool has_res = (p.flags & DMPQ_EP_RESIDUAL) != 0;
+        uint32_t g = 0;
+        for (int tile = ts0; tile < ts1; tile += tstep) {
+            const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;
+            const int row = mt * 256 + (int)rank * BM + q * 32 + lane;
+            const bool row_ok = row < p.m;
+            const float* sa_row = p.a_scale + (size_t)(row_ok ? row : 0) * p.num_kb;
+            f2 acc[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = f2make(0.0f, 0.0f);
+            float s_next = row_ok ? __ldg(sa_row) : 0.0f;
+            for (int kb = 0; kb < p.num_kb; ++kb, ++g) {
+                const uint32_t pb = g & 1u, pph = (g >> 1) & 1u;
+                const float s = s_next;
+                if (kb + 1 < p.num_kb && row_ok) s_next = __ldg(sa_row + kb + 1);
+                const f2 s2 = f2make(s, s);
+                mbar_wait(bar_pfull + 8 * pb, pph);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + pb * BN + csub * 64;
+                // four 16-column loads, each in flight while the previous one is promoted; the
+                // integer partial becomes a float exactly as bits(0x4B400000 + P) - 1.5 * 2^23
+                // (|P| < 2^22): an integer add and a packed subtract instead of two I2F
+                uint32_t r[2][16];
+                tmem_ld_32x32b_x16(taddr, r[0]);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    tmem_ld_wait();
+                    if (h < 3) tmem_ld_32x32b_x16(taddr + (h + 1) * 16, r[(h + 1) & 1]);
+                    if (h == 3) {   // the whole slice is in registers: release the partial to the MMA
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(leader_addr(bar_pempty + 8 * pb));
+                    }
+                    const f2 mg = f2make(12582912.0f, 12582912.0f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const f2 a = sub2(f2make(__int_as_float((int)r[h & 1][2 * i] + 0x4B400000),
+                                                 __int_as_float((int)r[h & 1][2 * i + 1] + 0x4B400000)), mg);
+                        acc[8 * h + i] = fma2(a, s2, acc[8 * h + i]);
+                    }
+                }
+            }
+            // output: y = fma(t, s_w[n], bias[n]), glue, bf16 / fp32 stores (lane = row)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col0 = nt * BN + csub * 64 + c * 32;
+                if (col0 >= p.n || !row_ok) continue;
+                f2 y[16];
+#pragma unroll
+                for (int v4 = 0; v4 < 8; ++v4) {
+                    const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.w_scale + col0) + v4);
+                    const float4 b4 = has_bias ? __ldg(reinterpret_cast<const float4*>(p.bias + col0) + v4)
+                                               : make_float4(-0.0f, -0.0f, -0.0f, -0.0f);
+                    y[2 * v4] = fma2(acc[16 * c + 2 * v4], f2make(w4.x, w4.y), f2make(b4.x, b4.y));
+                    y[2 * v4 + 1] = fma2(acc[16 * c + 2 * v4 + 1], f2make(w4.z, w4.w), f2make(b4.z, b4.w));
+                }
+                if (has_gelu) {
+                    const f2 k1 = f2make(0.044715f, 0.044715f), k0 = f2make(0.7978845608028654f, 0.7978845608028654f);
+                    const f2 hf = f2make(0.5f, 0.5f);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const f2 x = y[j];
+                        const f2 u = mul2(k0, fma2(k1, mul2(mul2(x, x), x), x));
+                        const f2 t = f2make(tanh_approx(f2lo(u)), tanh_approx(f2hi(u)));
+                        const f2 hh = mul2(hf, x);
+                        y[j] = fma2(hh, t, hh);
+                    }
+                }
+                if (has_res) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + (size_t)row * p.ldr + col0);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4) {
+                        const uint4 rv = __ldg(rp + v4);
+                        const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+                        const float4 ga = __ldg(reinterpret_cast<const float4*>(p.gate + col0) + 2 * v4);
+                        const float4 gb = __ldg(reinterpret_cast<const float4*>(p.gate + col0) + 2 * v4 + 1);
+                        const f2 gp[4] = {f2make(ga.x, ga.y), f2make(ga.z, ga.w), f2make(gb.x, gb.y), f2make(gb.z, gb.w)};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            y[v4 * 4 + j] = fma2(gp[j], y[v4 * 4 + j], f2make(bf16lo(w[j]), bf16hi(w[j])));
+                    }
+                }
+                if (p.Y) {
+                    uint4* yp = reinterpret_cast<uint4*>(p.Y + (size_t)row * p.ldy + col0);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4)
+                        yp[v4] = make_uint4(pack_bf16x2_f2(y[4 * v4]), pack_bf16x2_f2(y[4 * v4 + 1]),
+                                            pack_bf16x2_f2(y[4 * v4 + 2]), pack_bf16x2_f2(y[4 * v4 + 3]));
+                }
+                if (p.Y32) {
+                    float4* yp = reinterpret_cast<float4*>(p.Y32 + (size_t)row * p.n + col0);
+#pragma unroll
+                    for (int v4 = 0; v4 < 8; ++v4)
+                        yp[v4] = make_float4(f2lo(y[2 * v4]), f2hi(y[2 * v4]), f2lo(y[2 * v4 + 1]), f2hi(y[2 * v4 + 1]));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 2) tmem_dealloc_pair(tmem_base, 512);
+}
+
 // ------------------------------------------------------------------ host side
 
 
@@ -648,6 +906,27 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     return check_launch("dmpq_gemm");
 }
 
+static dmpq_status launch_gemm_i8b(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
+    using L = I8BLayout;
+    CUtensorMap tmA, tmB;
+    if (!make_tmap(&tmA, a_codes, p.m, p.kbytes, BM) || !make_tmap(&tmB, w_codes, p.n, p.kbytes, I8B_BN / 2))
+        return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (A/B)");
+    p.num_m_tiles = (p.m + 255) / 256;
+    p.num_n_tiles = (p.n + I8B_BN - 1) / I8B_BN;
+    p.num_kb = p.kbytes / BK_BYTES;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(dmpq_gemm_i8b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
+            return check_launch("dmpq_gemm(smem attribute, per-block INT8)");
+        attr_set = true;
+    }
+    const int tiles = p.num_m_tiles * p.num_n_tiles;
+    int clusters = num_sms() / 2;
+    if (clusters > tiles) clusters = tiles;
+    dmpq_gemm_i8b_kernel<<<2 * clusters, 128 + 32 * I8B_EPI_WARPS, L::TOTAL, s>>>(tmA, tmB, p);
+    return check_launch("dmpq_gemm(per-block INT8)");
+}
+
 }  // namespace dmpq
 
 using namespace dmpq;
@@ -690,6 +969,9 @@ extern "C" dmpq_status dmpq_prepare(void) {
     if (rc == DMPQ_OK) rc = set_pair_attrs<0, 256, 5, true>();   // fused TDC refresh variants
     if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5, true>();
     if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5, true>();
+    if (rc == DMPQ_OK && cudaFuncSetAttribute(dmpq_gemm_i8b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              I8BLayout::TOTAL) != cudaSuccess)
+        rc = check_launch("dmpq_prepare(per-block INT8 GEMM)");
     if (rc == DMPQ_OK) rc = prepare_quant_tma();
     if (rc == DMPQ_OK) rc = prepare_quant_had();
     return rc;
@@ -730,6 +1012,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.tdc_counter = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(ep->tdc_workspace) + kTdcPartialBytes);
     }
     p.Y = Y; p.ldy = ldy; p.Y32 = Y32; p.acc_out = acc_or_null;
+    if (ep) { p.run_if = ep->run_if; p.run_if_value = ep->run_if_value; }
     if (m == 0) {
         if (p.flags & DMPQ_EP_TDC_REFRESH) {   // empty sums
             if (cudaMemsetAsync(ep->tdc_stats, 0, 7 * sizeof(double), reinterpret_cast<cudaStream_t>(s)) != cudaSuccess)
@@ -764,6 +1047,12 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
                      DMPQ_EALIGN, "dmpq_gemm: INT8 operand pointers");
         p.kbytes = k;
         p.a_scale = A->row_scale; p.w_scale = W->i8_scale;
+        if (A->scale_block != 0) {   // per-block symmetric INT8 activations (R17)
+            DMPQ_REQUIRE(A->scale_block == 128 && k % 128 == 0, DMPQ_ESHAPE, "dmpq_gemm: per-block INT8 needs scale_block 128, k %% 128 == 0");
+            DMPQ_REQUIRE(!tdc && !acc_or_null, DMPQ_EUNSUPPORTED, "dmpq_gemm: per-block INT8 has no fused refresh / raw accumulators");
+            DMPQ_REQUIRE(!(p.flags & DMPQ_EP_RESIDUAL) || ep->ldr % 8 == 0, DMPQ_EALIGN, "dmpq_gemm: residual stride");
+            return launch_gemm_i8b(p, A->codes, W->i8_codes, st);
+        }
         if (tdc) return launch_gemm_pair<0, 256, 5, true>(p, A->codes, W->i8_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st)
                                  : launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);

@@ -118,6 +118,10 @@ extern "C" void dmpq_purify(const double* ratio, int n_layers, int prev_skipped,
     }
 }
 
+extern "C" double dmpq_outlier_ratio(double max_abs, double sum_abs, double count) {
+    return sum_abs > 0.0 ? max_abs / (sum_abs / count) : 1.0;
+}
+
 extern "C" void tdc_init(tdc_state* st) {
     st->t_p = -1;
     st->e_tp = INFINITY;

@@ -62,11 +62,15 @@ __global__ void __launch_bounds__(256) pack_int8_from_fp4_kernel(const uint8_t* 
     }
 }
 
-// g[0] *= f and s[0..n) *= f for an exact power of two f
-__global__ void scale_pow2_kernel(float* g, float* s, int n, float f) {
+// g[0] *= f and s[0..n) *= f for an exact power of two f; r[0..n) /= f (the cast's r_w: W^ scales
+// by f with g, so fl(W^ f * r_w / f) = fl(W^ r_w) keeps the INT8 codes)
+__global__ void scale_pow2_kernel(float* g, float* s, float* r, int n, float f) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) g[0] = __fmul_rn(g[0], f);
-    if (i < n) s[i] = __fmul_rn(s[i], f);
+    if (i < n) {
+        s[i] = __fmul_rn(s[i], f);
+        if (r) r[i] = __fdiv_rn(r[i], f);
+    }
 }
 
 }  // namespace dmpq
@@ -127,6 +131,6 @@ extern "C" dmpq_status dmpq_pack_weights_ex(const uint16_t* W, int n, int k, uin
     // R14: the packed forms above are those of U = W . blockdiag(H_128); the rotated weights are
     // W~ = 2^-7 U. Scaling by a power of two commutes with every rounding of the pack (E4M3/E2M1
     // codes are unchanged), so only g_w and the INT8 row scales take the factor (exactly).
-    scale_pow2_kernel<<<(n + 1 + 255) / 256, 256, 0, st>>>(out->fp4_g, out->i8_scale, n, 0.0078125f);
+    scale_pow2_kernel<<<(n + 1 + 255) / 256, 256, 0, st>>>(out->fp4_g, out->i8_scale, out->i8_rcp, n, 0.0078125f);
     return check_launch("dmpq_pack_weights(hadamard scale)");
 }

@@ -28,6 +28,24 @@ __global__ void __launch_bounds__(256) outlier_reduce_kernel(const float* rows, 
     }
 }
 
+// PDR current-input gate (R18): the outlier_reduce_kernel total (same order), then R and the flag
+__global__ void __launch_bounds__(256) outlier_gate_kernel(const float* rows, int m, const float* amax_in, double count,
+                                                           double tau, double* sum_out, int* flag_out) {
+    __shared__ double red[8];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) s = __dadd_rn(s, (double)rows[i]);
+    s = warp_sum_d(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = __dadd_rn(t, red[w]);
+        if (sum_out) *sum_out = t;
+        const double r = t > 0.0 ? __ddiv_rn((double)*amax_in, __ddiv_rn(t, count)) : 1.0;
+        *flag_out = r > tau ? 1 : 0;
+    }
+}
+
 __global__ void global_scale_kernel(const float* amax, float div, float* g_out, int count) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) {
@@ -54,6 +72,10 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
                      "dmpq_quantize_act: INT8 output descriptor mismatch");
         DMPQ_REQUIRE(out_i8->codes && out_i8->row_scale && aligned16(out_i8->codes), DMPQ_EALIGN,
                      "dmpq_quantize_act: INT8 output pointers");
+        DMPQ_REQUIRE(out_i8->scale_block == 0 || out_i8->scale_block == 128, DMPQ_EINVAL,
+                     "dmpq_quantize_act: INT8 scale_block must be 0 (per token) or 128 (per block)");
+        DMPQ_REQUIRE(out_i8->scale_block == 0 || (opts && (opts->flags & DMPQ_QF_HADAMARD)), DMPQ_EUNSUPPORTED,
+                     "dmpq_quantize_act: per-block INT8 (scale_block 128) is built for the Hadamard quantizer");
     }
     if (out_fp4) {
         DMPQ_REQUIRE(out_fp4->fmt == DMPQ_FMT_NVFP4 && out_fp4->m == m && out_fp4->k == k, DMPQ_ESHAPE,
@@ -74,6 +96,7 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
     }
     p.i8_codes = out_i8 ? reinterpret_cast<int8_t*>(out_i8->codes) : nullptr;
     p.i8_scale = out_i8 ? out_i8->row_scale : nullptr;
+    p.i8_block = out_i8 ? out_i8->scale_block : 0;
     p.fp4_codes = out_fp4 ? reinterpret_cast<uint8_t*>(out_fp4->codes) : nullptr;
     p.fp4_sf = out_fp4 ? out_fp4->sf : nullptr;
     p.g = out_fp4 ? out_fp4->g : nullptr;
@@ -88,7 +111,7 @@ extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ld
     if (p.flags & DMPQ_QF_HADAMARD) {
         // DMPQ_QUANT_HAD_CHUNK=1 selects the previous 64-element-chunk kernel (A/B measurements)
         static const bool chunk = [] { const char* e = getenv("DMPQ_QUANT_HAD_CHUNK"); return e && e[0] == '1'; }();
-        if (!chunk) return launch_quant_had(p, st);
+        if (!chunk || p.i8_block) return launch_quant_had(p, st);
     }
     return launch_quant_tma(p, (p.flags & DMPQ_QF_HADAMARD) != 0, st);
 }
@@ -99,6 +122,16 @@ extern "C" dmpq_status dmpq_outlier_reduce(const float* row_sums, int m, int seg
     DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_outlier_reduce: needs an sm_100 device");
     outlier_reduce_kernel<<<segments, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(row_sums, m, out);
     return check_launch("dmpq_outlier_reduce");
+}
+
+extern "C" dmpq_status dmpq_outlier_gate(const float* row_abs_sum, int m, const float* amax_in, double count,
+                                         double tau_outlier, double* sum_out, int* flag_out, dmpq_stream_t s) {
+    DMPQ_REQUIRE(row_abs_sum && amax_in && flag_out && m >= 0 && count > 0.0, DMPQ_EINVAL,
+                 "dmpq_outlier_gate: bad arguments");
+    DMPQ_REQUIRE(device_is_sm100(), DMPQ_EUNSUPPORTED, "dmpq_outlier_gate: needs an sm_100 device");
+    outlier_gate_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(row_abs_sum, m, amax_in, count, tau_outlier,
+                                                                          sum_out, flag_out);
+    return check_launch("dmpq_outlier_gate");
 }
 
 extern "C" dmpq_status dmpq_global_scale(const float* amax, float div, float* g_out, int count, dmpq_stream_t s) {

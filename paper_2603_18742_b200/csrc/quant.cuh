@@ -21,6 +21,7 @@ struct QuantParams {
     float* amax_out;
     float* row_abs_sum;   // PDR statistics (R15): per-row sum |x| of the layer input (pre-rotation)
     float* amax_in;       //                       max |x| of the layer input (pre-rotation)
+    int i8_block;   // INT8 scale granularity: 0 per token (R2), 128 per Hadamard block (R17)
     int kc4;     // scale-column atoms per 128-row tile: ceil(k/16/4)
     int m_pad;   // rows rounded up to 128 (scale rows to zero-fill)
 };

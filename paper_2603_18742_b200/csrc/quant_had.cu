@@ -140,7 +140,8 @@ __device__ __forceinline__ uint32_t int8x4_magic(f2 y01, f2 y23, f2 r2, f2 z2) {
 #ifndef DMPQ_HAD_LN_MINB
 #define DMPQ_HAD_LN_MINB 3   // CTAs per SM the LN variant is register-limited for (experiments)
 #endif
-// WH: write h (LN variants only). FMT: 1 NVFP4 only, 2 INT8 only, 3 both, 0 from the pointers.
+// WH: write h (LN variants only). FMT: 1 NVFP4 only, 2 INT8 only, 3 both, 0 from the pointers;
+// + 4: the INT8 output is per-block (one scale per thread's 128-block, R17) instead of per-token.
 template <bool LN, bool PDR, bool WH, int FMT = 0>
 __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_kernel(const QuantParams p, const __grid_constant__ CUtensorMap tmX,
                                                               int tpr, int R, int set_stride, int nbuf, int split) {
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
     const Seg8 sr{red, grp * (tpr >> 3), tpr >> 3};
     const bool want_fp4 = FMT ? (FMT & 1) != 0 : p.fp4_codes != nullptr;
     const bool want_i8 = FMT ? (FMT & 2) != 0 : p.i8_codes != nullptr;
+    const bool i8_block = FMT ? (FMT & 4) != 0 : p.i8_block != 0;
 
     // NVFP4 block-scale constants: raw = fl(fl(a/6)/g) takes the exact fast division when g is
     // in [2^-90, 2^90] and the block maxima in [a_lo, a_hi] (fastmath.cuh), else __fdiv_rn.
@@ -377,9 +379,15 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
             *reinterpret_cast<uint32_t*>(sp + 512) = s[2] | (s[3] << 16);
         }
         if (want_i8) {
-            const float am = sr.max(tmax, s0 + 2);
+            // per token: the row maximum over the CTA's segment reduction; per block (R17): this
+            // thread's own 128-block maximum, no reduction
+            const float am = i8_block ? tmax : sr.max(tmax, s0 + 2);
             const float rcp = am > 0.0f ? __fdiv_rn(127.0f, am) : 0.0f;
-            if (t == 0 && row_live) p.i8_scale[row] = am > 0.0f ? __fdiv_rn(am, 127.0f) : 1.0f;
+            if (i8_block) {
+                if (live) p.i8_scale[(size_t)row * nb + t] = am > 0.0f ? __fdiv_rn(am, 127.0f) : 1.0f;
+            } else if (t == 0 && row_live) {
+                p.i8_scale[row] = am > 0.0f ? __fdiv_rn(am, 127.0f) : 1.0f;
+            }
             if (live) {
                 const f2 r2 = f2make(rcp, rcp);
                 uint4* op = reinterpret_cast<uint4*>(p.i8_codes + (size_t)row * p.k + (size_t)t * 128);
@@ -475,7 +483,9 @@ dmpq_status prepare_quant_had() {
                              (const void*)quant_had_kernel<true, false, false, 2>,  (const void*)quant_had_kernel<true, false, false, 3>,
                              (const void*)quant_had_kernel<true, false, true>,      (const void*)quant_had_kernel<false, true, false>,
                              (const void*)quant_had_kernel<true, true, false>,      (const void*)quant_had_kernel<true, true, true>,
-                             (const void*)quant_had_kernel<false, false, false>,    (const void*)quant_had_kernel<true, false, false>};
+                             (const void*)quant_had_kernel<false, false, false>,    (const void*)quant_had_kernel<true, false, false>,
+                             (const void*)quant_had_kernel<false, false, false, 6>, (const void*)quant_had_kernel<false, false, false, 7>,
+                             (const void*)quant_had_kernel<true, false, false, 6>,  (const void*)quant_had_kernel<true, false, false, 7>};
     bool ok = true;
     for (const void* k : kernels)
         ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) == cudaSuccess;
@@ -521,8 +531,16 @@ dmpq_status launch_quant_had(const QuantParams& p, cudaStream_t s) {
     else {   // the common cases: formats fixed at compile time
         const int fmt = (p.fp4_codes ? 1 : 0) | (p.i8_codes ? 2 : 0);
 #define DMPQ_HAD_LAUNCH_F(a, f) quant_had_kernel<a, false, false, f><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split)
-        if (ln) { if (fmt == 1) DMPQ_HAD_LAUNCH_F(true, 1); else if (fmt == 2) DMPQ_HAD_LAUNCH_F(true, 2); else if (fmt == 3) DMPQ_HAD_LAUNCH_F(true, 3); else DMPQ_HAD_LAUNCH(true, false, false); }
-        else { if (fmt == 1) DMPQ_HAD_LAUNCH_F(false, 1); else if (fmt == 2) DMPQ_HAD_LAUNCH_F(false, 2); else if (fmt == 3) DMPQ_HAD_LAUNCH_F(false, 3); else DMPQ_HAD_LAUNCH(false, false, false); }
+        const int f = fmt | (p.i8_codes && p.i8_block ? 4 : 0);
+        if (ln) {
+            if (f == 1) DMPQ_HAD_LAUNCH_F(true, 1); else if (f == 2) DMPQ_HAD_LAUNCH_F(true, 2);
+            else if (f == 3) DMPQ_HAD_LAUNCH_F(true, 3); else if (f == 6) DMPQ_HAD_LAUNCH_F(true, 6);
+            else if (f == 7) DMPQ_HAD_LAUNCH_F(true, 7); else DMPQ_HAD_LAUNCH(true, false, false);
+        } else {
+            if (f == 1) DMPQ_HAD_LAUNCH_F(false, 1); else if (f == 2) DMPQ_HAD_LAUNCH_F(false, 2);
+            else if (f == 3) DMPQ_HAD_LAUNCH_F(false, 3); else if (f == 6) DMPQ_HAD_LAUNCH_F(false, 6);
+            else if (f == 7) DMPQ_HAD_LAUNCH_F(false, 7); else DMPQ_HAD_LAUNCH(false, false, false);
+        }
 #undef DMPQ_HAD_LAUNCH_F
     }
 #undef DMPQ_HAD_LAUNCH

@@ -182,8 +182,11 @@ class QuantAct:
     row_scale: torch.Tensor | None = None
     c: L.Act = field(default=None, repr=False)
 
+    scale_block: int = 0
+
     @classmethod
-    def empty(cls, fmt: int, m: int, k: int, device, g: torch.Tensor | None = None):
+    def empty(cls, fmt: int, m: int, k: int, device, g: torch.Tensor | None = None, scale_block: int = 0):
+        """scale_block (INT8 only): 0 per-token scales [m] (R2); 128 per-block scales [m, k/128] (R17)."""
         d = dict(device=device)
         if fmt == FMT_NVFP4:
             if g is None:
@@ -192,9 +195,12 @@ class QuantAct:
                     sf=torch.empty(sf_bytes(m, k), dtype=torch.uint8, **d), g=g)
             a.c = L.Act(fmt, m, k, a.codes.data_ptr(), a.sf.data_ptr(), g.data_ptr(), None)
         else:
+            if scale_block not in (0, 128) or (scale_block and k % scale_block):
+                raise ValueError("scale_block must be 0 or 128 (dividing k)")
             a = cls(fmt, m, k, torch.empty((m, k), dtype=torch.int8, **d),
-                    row_scale=torch.empty(m, dtype=torch.float32, **d))
-            a.c = L.Act(fmt, m, k, a.codes.data_ptr(), None, None, a.row_scale.data_ptr())
+                    row_scale=torch.empty((m, k // scale_block) if scale_block else m, dtype=torch.float32, **d),
+                    scale_block=scale_block)
+            a.c = L.Act(fmt, m, k, a.codes.data_ptr(), None, None, a.row_scale.data_ptr(), scale_block)
         return a
 
     @classmethod
@@ -240,6 +246,20 @@ def dmpq_outlier_reduce(row_sums: torch.Tensor, out: torch.Tensor):
     return out
 
 
+def dmpq_outlier_ratio(max_abs: float, sum_abs: float, count: float) -> float:
+    """R = max|x| / mean|x|; 1 for an all-zero input."""
+    return float(L.lib().dmpq_outlier_ratio(float(max_abs), float(sum_abs), float(count)))
+
+
+def dmpq_outlier_gate(row_abs_sum: torch.Tensor, amax_in: torch.Tensor, count: float, tau_outlier: float,
+                      flag_out: torch.Tensor, sum_out: torch.Tensor | None = None):
+    """Current-input PDR gate on the device (R18): flag_out[0] = R > tau_outlier."""
+    L.check("dmpq_outlier_gate", L.lib().dmpq_outlier_gate(
+        _ptr(row_abs_sum), row_abs_sum.numel(), _ptr(amax_in), float(count), float(tau_outlier), _ptr(sum_out),
+        _ptr(flag_out), _stream(row_abs_sum.device)))
+    return flag_out
+
+
 def dmpq_purify(fmts, ratios, prev_skipped: bool, tau_outlier: float = 25.0):
     """Purified Cache Refresh gate (R15): BF16 if ratio > tau_outlier, INT8 after a skip."""
     n = len(fmts)
@@ -263,7 +283,8 @@ def dmpq_gemm(A: QuantAct, W: PackedWeights, Y: torch.Tensor | None = None, Y32:
               acc: torch.Tensor | None = None, bias: bool = True, gelu: bool = False,
               residual: torch.Tensor | None = None, gate: torch.Tensor | None = None,
               tdc_x_in: torch.Tensor | None = None, tdc_delta: torch.Tensor | None = None,
-              tdc_stats: torch.Tensor | None = None, tdc_workspace: torch.Tensor | None = None):
+              tdc_stats: torch.Tensor | None = None, tdc_workspace: torch.Tensor | None = None,
+              run_if: torch.Tensor | None = None, run_if_value: int = 0):
     """Y = epilogue(A @ W^T) on tcgen05 (kind::i8 or kind::mxf4nvf4). With tdc_x_in / tdc_delta /
     tdc_stats / tdc_workspace the epilogue also runs the TDC refresh of X_out = Y (fused tdc_step)."""
     flags = (L.EP_BIAS if (bias and W.bias is not None) else 0) | (L.EP_GELU_TANH if gelu else 0)
@@ -274,9 +295,10 @@ def dmpq_gemm(A: QuantAct, W: PackedWeights, Y: torch.Tensor | None = None, Y32:
         for t_, n_ in ((tdc_x_in, "tdc_x_in"), (tdc_delta, "tdc_delta")):
             _check_dev(t_, n_, torch.bfloat16)
     ep = None
-    if flags:
+    if flags or run_if is not None:   # run_if: int32 device flag, the GEMM runs iff *run_if == run_if_value (R18)
         ep = L.Epilogue(flags, _ptr(gate), _ptr(residual), 0 if residual is None else residual.stride(0),
-                        _ptr(tdc_x_in), _ptr(tdc_delta), _ptr(tdc_stats), _ptr(tdc_workspace))
+                        _ptr(tdc_x_in), _ptr(tdc_delta), _ptr(tdc_stats), _ptr(tdc_workspace), _ptr(run_if),
+                        int(run_if_value))
     if Y is not None:
         _check_dev(Y, "Y", torch.bfloat16)
     L.check("dmpq_gemm", L.lib().dmpq_gemm(

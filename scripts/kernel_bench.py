@@ -33,18 +33,18 @@ def timeit(fn, iters=20, warmup=3):
     return s.elapsed_time(e) / iters * 1e-3
 
 
-def bench_gemm(m, n, k, fmt, nbuf=2):
+def bench_gemm(m, n, k, fmt, nbuf=2, block=0):
     x = synth.dit_activation(m, k, seed=1).cuda()
     w, b = synth.linear_weight(n, k, seed=2)
-    pw = D.dmpq_pack_weights(w.cuda(), b)
+    pw = D.dmpq_pack_weights(w.cuda(), b, hadamard=bool(block))
     g = torch.tensor([1e-3], device="cuda")
     acts = []
     for i in range(nbuf):
-        a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == D.FMT_NVFP4 else None)
+        a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == D.FMT_NVFP4 else None, scale_block=block)
         if fmt == D.FMT_NVFP4:
             D.dmpq_quantize_act(x, out_fp4=a)
         else:
-            D.dmpq_quantize_act(x, out_i8=a)
+            D.dmpq_quantize_act(x, out_i8=a, hadamard=bool(block))
         acts.append(a)
     ys = [torch.empty(m, n, dtype=torch.bfloat16, device="cuda") for _ in range(nbuf)]
     it = [0]
@@ -56,7 +56,8 @@ def bench_gemm(m, n, k, fmt, nbuf=2):
     t = timeit(run)
     flops = 2.0 * m * n * k
     peak = PEAKS["bf16_tflops"] * (4 if fmt == D.FMT_NVFP4 else 2)
-    return dict(kernel="gemm_" + ("nvfp4" if fmt == D.FMT_NVFP4 else "int8"), m=m, n=n, k=k, us=t * 1e6,
+    return dict(kernel="gemm_" + ("nvfp4" if fmt == D.FMT_NVFP4 else "int8") + ("_block" if block else ""), m=m, n=n, k=k,
+                us=t * 1e6,
                 tflops=flops / t / 1e12, frac=flops / t / 1e12 / peak)
 
 
@@ -110,6 +111,7 @@ def main():
     ap.add_argument("--quant", action="store_true")
     ap.add_argument("--tdc", action="store_true")
     ap.add_argument("--shapes", default="c2,c4")
+    ap.add_argument("--block", action="store_true", help="also the per-block INT8 GEMM (R17)")
     ap.add_argument("--one", default=None, help="fmt:m,n,k  e.g. nvfp4:35552,3072,3072 (one GEMM, 5 launches)")
     a = ap.parse_args()
     if a.one:
@@ -129,8 +131,10 @@ def main():
         if "c4" in a.shapes:
             shapes += [(35552, 3072, 3072), (35552, 12288, 3072), (35552, 3072, 12288)]
         for (m, n, k) in shapes:
-            for fmt in (D.FMT_NVFP4, D.FMT_INT8):
-                r = bench_gemm(m, n, k, fmt)
+            for fmt, blk in ((D.FMT_NVFP4, 0), (D.FMT_INT8, 0), (D.FMT_INT8, 128)):
+                if blk and not a.block:
+                    continue
+                r = bench_gemm(m, n, k, fmt, block=blk)
                 print(json.dumps(r), flush=True)
                 res.append(r)
     if a.quant:

@@ -156,3 +156,19 @@ def test_predict_l2_metric_matches_oracle(L, orc):
     assert dmpq.dmpq_predict(st, [0.6], 3, False)[1] == 0.5
     assert dmpq.dmpq_predict(st, [0.6], 3, False, metric=L.GAMMA_L2)[1] == pytest.approx(2 ** -0.5, rel=1e-15)
     assert dmpq.dmpq_predict(st, [0.6], 3, False, metric=L.GAMMA_L2)[0] == [orc.FMT_INT8]
+
+
+def test_outlier_ratio_matches_oracle(L, orc):
+    """dmpq_outlier_ratio (host-pure, P:241 R = max|X| / mean|X|) equals the oracle's ratio computed
+    from the same tensor, and is 1 for an all-zero input."""
+    from paper_2603_18742_b200 import dmpq
+    rng = np.random.default_rng(5)
+    for trial in range(50):
+        x = (rng.standard_normal(777) * rng.choice([1.0, 40.0], size=777, p=[0.99, 0.01])).astype(np.float32)
+        import torch
+        b = torch.from_numpy(x).to(torch.bfloat16)
+        bits = b.view(torch.int16).numpy().view(np.uint16)
+        xf = np.abs(b.float().numpy().astype(np.float64))
+        got = dmpq.dmpq_outlier_ratio(float(xf.max()), float(xf.sum()), x.size)
+        assert got == pytest.approx(orc.outlier_ratio(bits), rel=1e-12)
+    assert dmpq.dmpq_outlier_ratio(0.0, 0.0, 100) == 1.0

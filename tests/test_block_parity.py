@@ -41,11 +41,18 @@ MODES = {
     "dmpq_tdc": (False, False, 25.0, False, 0.003),
     "dmpq_tdc_fused_refresh": (False, False, 25.0, False, 0.003, True),
     "hadamard_pdr": (True, True, 9.0, False, 0.003),   # tau_outlier between the O-input and FFN2-input ratios: mixed BF16
+    # every ratio exceeds 1: all layers BF16 after t = 0, incl. the O projection, whose input V is then
+    # written densely instead of into the strided Q|K|V buffer (the BF16 GEMM reads A with row stride k)
+    "hadamard_pdr_all_bf16": (True, True, 1.0, False, 0.003),
+    # the paper-literal gate: R of THIS step's layer input, decided on the device (R18)
+    "hadamard_pdr_current": (True, "current", 9.0, False, 0.003),
     # the compressed cache's quantization noise enters Eq. 9 (E >= ~eps^2/2 ~ 0.004 here, R16): a looser tau
     # so that the trajectory still skips
     "hadamard_cache_nvfp4": (True, False, 25.0, True, 0.02),
     # NVFP4-only weight residency, INT8 codes cast on the fly per INT8 GEMM (NEXT-4b)
     "hadamard_int8_cast": (True, False, 25.0, False, 0.02, False, True),
+    # per-block symmetric INT8 over the Hadamard blocks (R17, NEXT-1)
+    "hadamard_int8_block": (True, False, 25.0, False, 0.02, False, False, True),
 }
 
 
@@ -68,9 +75,10 @@ def run(request):
     had, pdr, tau_o, c4, tau_c = MODES[request.param][:5]
     fused = len(MODES[request.param]) > 5 and MODES[request.param][5]
     cast = len(MODES[request.param]) > 6 and MODES[request.param][6]
+    i8b = len(MODES[request.param]) > 7 and MODES[request.param][7]
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
     stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o,
-                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused, int8_cast=cast)
+                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused, int8_cast=cast, int8_block=i8b)
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):
@@ -109,7 +117,10 @@ def _check_quant(orc, src_bf16, act, fmt, k, had=False):
         assert np.array_equal(act["codes"].cpu().numpy(), c)
         assert np.array_equal(orc.sf_unswizzle(act["sf"].cpu().numpy(), m, k), s)
         return c, s, g
-    c, s = orc.int8_quantize_f32(y) if had else orc.int8_quantize(bits(src_bf16))
+    if act["row_scale"].dim() == 2:   # per-block INT8 (R17)
+        c, s = orc.int8_quantize_blocks_f32(y)
+    else:
+        c, s = orc.int8_quantize_f32(y) if had else orc.int8_quantize(bits(src_bf16))
     assert np.array_equal(act["codes"].cpu().numpy(), c)
     assert np.array_equal(act["row_scale"].cpu().numpy(), s)
     return c, s, None
@@ -129,6 +140,8 @@ def _gemm_ref(orc, fmt, q, pw, n, k):
     if pw.i8_codes is None:   # NVFP4-only residency: the INT8 codes the cast rebuilds (cast parity: test_gpu_parity)
         pw = D.dmpq_cast_int8(pw, torch.empty(pw.n * pw.k, dtype=torch.int8, device="cuda"))
         torch.cuda.synchronize()
+    if s.ndim == 2:   # per-block INT8 (R17): FP32-promoted partial sums, a tolerance path like NVFP4
+        return orc.gemm_int8_blocks(c, s, pw.i8_codes.cpu().numpy(), pw.i8_scale.cpu().numpy(), bias), False
     _, y = orc.gemm_int8(c, s, pw.i8_codes.cpu().numpy(), pw.i8_scale.cpu().numpy(), bias)
     return y.astype(np.float64), True
 
@@ -232,9 +245,13 @@ def test_decisions_match_oracle(run, orc):
             gamma = None if prev_stats is None else orc.gamma_from_stats(prev_stats)
             ref = orc.route_block(gamma, stack.tau, t, prev_skipped)
             slot_of = (0, 0, 0, 1, 2, 3)
+            cur = None
+            if stack.pdr_current:   # R of this step's layer inputs (h1, V, h2, f), from the GPU's stage inputs
+                cap = st["cap"]
+                cur = [orc.outlier_ratio(bits(cap[k_])) for k_ in ("h1", "y2", "h2", "f")]
             for j, (a, b) in enumerate(zip(ref, st["fmts"])):
-                if stack.pdr and st["ratio"] is not None:
-                    r = st["ratio"][slot_of[j]]
+                if stack.pdr and (cur is not None or st["ratio"] is not None):
+                    r = (cur if cur is not None else st["ratio"])[slot_of[j]]
                     if abs(r - stack.tau_outlier) <= 1e-6 * stack.tau_outlier:
                         continue
                     a = orc.purify_route(a, r, prev_skipped, stack.tau_outlier)

@@ -644,3 +644,92 @@ def test_cast_int8_concatenated(D, orc):
     c = D.dmpq_cast_int8(cat, scratch)
     torch.cuda.synchronize()
     assert torch.equal(c.i8_codes.cpu(), torch.cat([f.i8_codes for f in fulls]).cpu())
+
+
+@pytest.mark.parametrize("m,k", [(300, 1920), (129, 3072), (5, 12288)])
+def test_outlier_gate_current_input(D, orc, m, k):
+    """The device-side PDR gate (R18): its FP64 sum equals dmpq_outlier_reduce's, and its
+    decision equals R > tau for the oracle's outlier ratio of the same input, for thresholds just
+    below and above R (strict inequality) and far from it; a predicated GEMM pair runs exactly one."""
+    x = synth.dit_activation(m, k, seed=m * 3 + k)
+    a8 = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda")
+    rs = torch.zeros(1, m, dtype=torch.float32, device="cuda")
+    ain = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(x.cuda(), out_i8=a8, hadamard=True, row_abs_sum=rs[0], amax_in=ain)
+    tot = torch.zeros(1, dtype=torch.float64, device="cuda")
+    D.dmpq_outlier_reduce(rs, tot)
+    torch.cuda.synchronize()
+    r_ref = orc.outlier_ratio(synth.bits(x))
+    r_dev = D.dmpq_outlier_ratio(ain.item(), tot.item(), m * k)
+    assert r_dev == pytest.approx(r_ref, rel=1e-5)
+    for tau in (r_dev * (1 - 1e-9), r_dev * (1 + 1e-9), 1.0, 1e6, 25.0):
+        flag = torch.full((1,), 7, dtype=torch.int32, device="cuda")
+        s_out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        D.dmpq_outlier_gate(rs[0], ain, m * k, tau, flag, s_out)
+        torch.cuda.synchronize()
+        assert s_out.item() == tot.item()
+        assert flag.item() == int(r_dev > tau), (tau, r_dev)
+        if abs(r_ref - tau) > 1e-5 * tau:
+            assert flag.item() == int(r_ref > tau)
+    # predicated launches: exactly the GEMM whose run_if_value matches the flag writes its output
+    w, b = synth.linear_weight(64, k, seed=3)
+    pw = D.dmpq_pack_weights(w.cuda(), b, keep_bf16=True)
+    flag = torch.ones(1, dtype=torch.int32, device="cuda")
+    y_q = torch.full((m, 64), float("nan"), device="cuda")
+    y_b = torch.full((m, 64), float("nan"), device="cuda")
+    D.dmpq_gemm(a8, pw, Y32=y_q, run_if=flag, run_if_value=0)
+    D.dmpq_gemm(D.QuantAct.bf16(x.cuda()), pw, Y32=y_b, run_if=flag, run_if_value=1)
+    torch.cuda.synchronize()
+    assert torch.isnan(y_q).all() and not torch.isnan(y_b).any()
+
+
+@pytest.mark.parametrize("m,k,ln", [(5, 128, False), (1029, 3072, True), (300, 1920, False), (33, 12288, False)])
+def test_quantize_int8_blocks_bit_exact(D, orc, m, k, ln):
+    """Per-block symmetric INT8 over the 128-element Hadamard blocks (R17): codes and the
+    [m, k/128] block scales bit-exact against the oracle on the FP32 FHT output (also with LN and
+    the NVFP4 output in the same pass), adversarial rows included."""
+    x = torch.cat([synth.dit_activation(m, k, seed=m + 5 * k), synth.adversarial_rows(k)])
+    mm = x.shape[0]
+    h = torch.empty(mm, k, dtype=torch.bfloat16, device="cuda") if ln else None
+    g = torch.tensor([0.01], device="cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, mm, k, "cuda", g=g)
+    for with_fp4 in (False, True):
+        a8 = D.QuantAct.empty(D.FMT_INT8, mm, k, "cuda", scale_block=128)
+        D.dmpq_quantize_act(x.cuda(), out_i8=a8, out_fp4=a4 if with_fp4 else None, layernorm=ln, h_out=h, hadamard=True)
+        torch.cuda.synchronize()
+        src = synth.bits(h.cpu()) if ln else synth.bits(x)
+        y = orc.fht128(orc.bf16_to_f32(src).reshape(mm, k))
+        c8, s8 = orc.int8_quantize_blocks_f32(y)
+        assert np.array_equal(a8.row_scale.cpu().numpy(), s8)
+        assert np.array_equal(a8.codes.cpu().numpy(), c8)
+        if with_fp4:
+            c4, s4 = orc.nvfp4_quantize_f32(y, 0.01)
+            assert np.array_equal(a4.codes.cpu().numpy(), c4)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 192, 128), (300, 384, 256), (257, 1920, 1920), (1029, 3072, 3072), (64, 96, 12288)])
+def test_gemm_int8_blocks_rel_l2(D, orc, m, n, k):
+    """Per-block INT8 GEMM (R17): exact integer partial per 128-K block, FP32 promotion with the block
+    scale: fp32 output within rel-L2 1e-5 of the oracle's FP64 (exact per-block sums, FP64 scaling),
+    bf16 output the RNE of it; bias, GELU and gated-residual glue as the other kinds."""
+    x = synth.dit_activation(m, k, seed=7 * m + k)
+    w, b = synth.linear_weight(n, k, seed=n + 9 * k)
+    pw = D.dmpq_pack_weights(w.cuda(), b, hadamard=True)
+    a = D.QuantAct.empty(D.FMT_INT8, m, k, "cuda", scale_block=128)
+    D.dmpq_quantize_act(x.cuda(), out_i8=a, hadamard=True)
+    y32 = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y, Y32=y32)
+    res = synth.dit_activation(m, n, seed=m + 1, outlier_frac=0, tail_frac=0).cuda()
+    gate = (0.05 * torch.rand(n, generator=torch.Generator().manual_seed(n))).cuda()
+    y32r = torch.empty(m, n, dtype=torch.float32, device="cuda")
+    D.dmpq_gemm(a, pw, Y32=y32r, residual=res, gate=gate)
+    torch.cuda.synchronize()
+    ref = orc.gemm_int8_blocks(a.codes.cpu().numpy(), a.row_scale.cpu().numpy(), pw.i8_codes.cpu().numpy(),
+                               pw.i8_scale.cpu().numpy(), b.numpy())
+    assert rel_l2(y32.cpu().numpy(), ref) <= 1e-5
+    assert torch.equal(y.cpu(), y32.cpu().to(torch.bfloat16))
+    yp = y32.cpu().numpy().astype(np.float64)
+    got = y32r.cpu().numpy().astype(np.float64)
+    want = gate.cpu().numpy().astype(np.float64)[None, :] * yp + res.cpu().float().numpy().astype(np.float64)
+    assert np.all(np.abs(got - want) <= np.abs(want) * 2.0 ** -23 + 1e-30)
