@@ -264,6 +264,7 @@ dmpq_status dmpq_global_scale(const float* amax, float div, float* g_out, int co
 #define DMPQ_EP_GELU_TANH 2u  /* y = gelu_tanh(y)  (block glue)                        */
 #define DMPQ_EP_RESIDUAL  4u  /* y = residual[m,n] + gate[n] * y (gated residual glue) */
 #define DMPQ_EP_TDC_REFRESH 8u /* fused TDC refresh of the stored bf16 Y (= X_out), below */
+#define DMPQ_EP_QUANT_NVFP4 16u /* producer-fused NVFP4 quantization of bf16(Y) for the next layer, below */
 
 typedef struct {
     uint32_t flags;
@@ -289,6 +290,15 @@ typedef struct {
      * outlier gate (dmpq_outlier_gate) picks the one that runs. */
     const int* run_if;
     int run_if_value;
+    /* DMPQ_EP_QUANT_NVFP4 (quantization "fused directly into the preceding layers"; NEXT-2):
+     * the epilogue also quantizes the bf16 output it produces, v = bf16(y) after every glue step,
+     * to NVFP4 exactly as dmpq_quantize_act does without the Hadamard option (Eq. 2, R3/R4: block
+     * scale E4M3(fl(fl(a_b/6)/g)), codes E2M1(fl(v fl(1/eff)))): codes and swizzled scales go to
+     * q_out (NVFP4 descriptor with q_out->m == m, q_out->k == n, its g = the consumer's global scale;
+     * scale rows m..ceil128(m) are zeroed) and max|v| is max-reduced into *q_amax (device, caller
+     * zeroes). Y may then be NULL (the bf16 tensor is not stored). n % 64 == 0. */
+    const dmpq_act* q_out;
+    float* q_amax;
 } dmpq_epilogue;
 
 /* Workspace bytes of the fused TDC refresh (DMPQ_EP_TDC_REFRESH) on the current device. */

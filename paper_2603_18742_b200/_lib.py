@@ -21,7 +21,7 @@ STATUS_NAMES = ["DMPQ_OK", "DMPQ_EINVAL", "DMPQ_ESHAPE", "DMPQ_EALIGN", "DMPQ_EZ
 FMT_INT8, FMT_NVFP4, FMT_BF16 = 0, 1, 2
 QF_LAYERNORM, QF_WRITE_H, QF_HADAMARD = 1, 2, 4
 PACK_HADAMARD = 1
-EP_BIAS, EP_GELU_TANH, EP_RESIDUAL, EP_TDC_REFRESH = 1, 2, 4, 8
+EP_BIAS, EP_GELU_TANH, EP_RESIDUAL, EP_TDC_REFRESH, EP_QUANT_NVFP4 = 1, 2, 4, 8, 16
 TDC_SKIP, TDC_REFRESH = 0, 1
 TDC_COMPUTE, TDC_DECIDE_SKIP = 0, 1
 GAMMA_L1, GAMMA_L2 = 0, 1
@@ -47,7 +47,7 @@ class QuantOpts(ctypes.Structure):
 class Epilogue(ctypes.Structure):
     _fields_ = [("flags", c_uint32), ("gate", c_void_p), ("residual", c_void_p), ("ldr", c_int),
                 ("tdc_x_in", c_void_p), ("tdc_delta", c_void_p), ("tdc_stats", c_void_p), ("tdc_workspace", c_void_p),
-                ("run_if", c_void_p), ("run_if_value", c_int)]
+                ("run_if", c_void_p), ("run_if_value", c_int), ("q_out", c_void_p), ("q_amax", c_void_p)]
 
 
 class BlockStats(ctypes.Structure):

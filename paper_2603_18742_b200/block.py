@@ -129,7 +129,8 @@ class DiTStack:
                  tdc_cfg=(0.001, 0.003, 2), tau_gamma=None, gate_scales=None, tdc_enabled: bool = True,
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
                  tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False,
-                 fuse_refresh: bool = False, fuse_qkv: bool = True, int8_cast: bool = False, int8_block: bool = False):
+                 fuse_refresh: bool = False, fuse_qkv: bool = True, int8_cast: bool = False, int8_block: bool = False,
+                 fuse_quant: bool = False):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -158,6 +159,10 @@ class DiTStack:
         if int8_block and not hadamard:
             raise ValueError("per-block INT8 (R17) is defined on the Hadamard blocks: needs hadamard=True")
         self.int8_block = int8_block
+        # producer-fused quantization (NEXT-2): FFN1's epilogue writes the NVFP4 codes of the
+        # FFN2 input directly (no bf16 f round trip, no standalone quantizer) when FFN2 is routed
+        # NVFP4; built for the plain quantizer (the Hadamard blocks do not fit the epilogue, DESIGN 5.7)
+        self.fuse_quant = fuse_quant and not hadamard and not pdr
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
         self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr,
@@ -337,9 +342,17 @@ class DiTStack:
             self._cap("h2", ws.h2)
             if fmts[4] != D.FMT_BF16:
                 self._cap_act("a2", q2[fmts[4]])
-        self._gemm(q2[fmts[4]], W.layers[4], Y=ws.f, gelu=True)
+        if self.fuse_quant and fmts[5] == D.FMT_NVFP4:
+            a3 = ws.act(3, D.FMT_NVFP4, b)
+            self._gemm(q2[fmts[4]], W.layers[4], Y=ws.f if cap else None, gelu=True, quant_out=a3,
+                       quant_amax=self.amax[0, b, 3:4])
+            q3 = {D.FMT_NVFP4: a3}
+        else:
+            self._gemm(q2[fmts[4]], W.layers[4], Y=ws.f, gelu=True)
+            q3 = None
         self._cap("f", ws.f)
-        q3 = self._quant(b, 3, ws.f, {fmts[5]})
+        if q3 is None:
+            q3 = self._quant(b, 3, ws.f, {fmts[5]})
         if fmts[5] != D.FMT_BF16:
             self._cap_act("a3", q3[fmts[5]])
         tdc = {}
@@ -470,6 +483,8 @@ class DiTStack:
             else:   # 4 quantizers + 6 GEMMs + refresh, fewer when fused, +2 for a cache bootstrap
                 qkv1 = self.fuse_qkv and fmts[0] == fmts[1] == fmts[2] and fmts[3] != D.FMT_BF16 and not self.pdr_current
                 self.launches += 11 - (1 if self.fuse_refresh else 0) - (2 if qkv1 else 0) + (2 if first else 0)
+                if self.fuse_quant and fmts[5] == D.FMT_NVFP4:   # FFN2's quantizer runs inside FFN1
+                    self.launches -= 1
                 if self.pdr_current:   # + 4 device gates + the predicated-off GEMM of every layer
                     self.launches += 4 + 6
                 if self.int8_cast:   # one cast per INT8 GEMM launch

@@ -63,6 +63,12 @@ struct GemmParams {
     // device-predicated launch (R18): run only when *run_if == run_if_value
     const int* run_if;
     int run_if_value;
+    // producer-fused NVFP4 quantization of bf16(Y) (DMPQ_EP_QUANT_NVFP4)
+    uint8_t* q_codes;
+    uint8_t* q_sf;
+    const float* q_g;
+    float* q_amax;
+    int q_kc4, q_m_pad;
 };
 
 constexpr int BM = 128;
@@ -123,7 +129,7 @@ struct PairLayout {
     static_assert(TOTAL <= SMEM_LIMIT, "shared memory budget");
 };
 
-template <int KIND, int BN, int STAGES, bool TDC = false>   // TDC: fused refresh epilogue compiled in
+template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false>   // TDC: fused refresh; QNT: fused NVFP4 quantizer
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     dmpq_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
@@ -320,6 +326,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         const bool has_tdc = TDC && (p.flags & DMPQ_EP_TDC_REFRESH) != 0;
         // fused TDC refresh statistics of this warp's rows / chunks over all its tiles (fixed order)
         double tacc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const float qg = QNT ? *p.q_g : 1.0f;   // the consumer's NVFP4 global scale (R3)
+        float qamax = 0.0f;
         for (int tile = ts0; tile < ts1; tile += tstep, ++local) {
             const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int acc = local & 1;
@@ -478,6 +486,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                 uint32_t yb[16];   // the stored bf16 output (X_out for the fused TDC refresh)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) yb[j] = pack_bf16x2_f2(y[j]);
+                if constexpr (QNT) {
+                    // producer-fused NVFP4 quantization of v = bf16(y) (Eq. 2, R3/R4, IEEE block-scale
+                    // arithmetic = dmpq_quantize_act's): two 16-element blocks per 32-column chunk
+                    if (row < p.q_m_pad) {
+                        uint32_t sc = 0;
+                        if (row_ok) {
+                            uint32_t cw[4];
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                float a = 0.0f;
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    a = fmaxf(a, fmaxf(fabsf(bf16lo(yb[8 * h + j])), fabsf(bf16hi(yb[8 * h + j]))));
+                                const uint32_t sb = e4m3_rn_satfinite(__fdiv_rn(__fdiv_rn(a, 6.0f), qg));
+                                const float eff = __fmul_rn(e4m3_decode(sb), qg);
+                                const float rq = eff > 0.0f ? __frcp_rn(eff) : 0.0f;
+                                const f2 r2 = f2make(rq, rq);
+                                f2 v[8];
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) v[j] = mul2(f2make(bf16lo(yb[8 * h + j]), bf16hi(yb[8 * h + j])), r2);
+                                cw[2 * h] = e2m1x8(v[0], v[1], v[2], v[3]);
+                                cw[2 * h + 1] = e2m1x8(v[4], v[5], v[6], v[7]);
+                                sc |= sb << (8 * h);
+                                qamax = fmaxf(qamax, a);
+                            }
+                            *reinterpret_cast<uint4*>(p.q_codes + (size_t)row * (p.n >> 1) + (col0 >> 1)) =
+                                make_uint4(cw[0], cw[1], cw[2], cw[3]);
+                        }
+                        *reinterpret_cast<uint16_t*>(sf_row_ptr(p.q_sf, p.q_kc4, row) + (size_t)(col0 >> 6) * 512 +
+                                                     ((col0 >> 4) & 3)) = (uint16_t)sc;
+                    }
+                }
                 if (p.Y) {
                     if (!tma_res) {
                         if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
@@ -586,6 +626,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     *p.tdc_counter = 0u;   // ready for the next call
                 }
             }
+        }
+        if constexpr (QNT) {
+            qamax = warp_max(qamax);
+            if (lane == 0) atomic_max_nonneg(p.q_amax, qamax);
         }
         if (lane == 0) bulk_wait_all();
     }
@@ -730,26 +774,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * I8B_EPI_W
                 mbar_wait(bar_pfull + 8 * pb, pph);
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + pb * BN + csub * 64;
-                // four 16-column loads, each in flight while the previous one is promoted; the
-                // integer partial becomes a float exactly as bits(0x4B400000 + P) - 1.5 * 2^23
-                // (|P| < 2^22): an integer add and a packed subtract instead of two I2F
-                uint32_t r[2][16];
-                tmem_ld_32x32b_x16(taddr, r[0]);
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
+                for (int h = 0; h < 2; ++h) {
+                    // (measured: four pipelined 16-column loads with an integer-add / subtract
+                    // conversion instead of I2F were 18 % slower -- the promotion is issue-bound)
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(taddr + h * 32, r);
                     tmem_ld_wait();
-                    if (h < 3) tmem_ld_32x32b_x16(taddr + (h + 1) * 16, r[(h + 1) & 1]);
-                    if (h == 3) {   // the whole slice is in registers: release the partial to the MMA
+                    if (h == 1) {   // both halves in registers: release the partial to the MMA
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(leader_addr(bar_pempty + 8 * pb));
                     }
-                    const f2 mg = f2make(12582912.0f, 12582912.0f);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const f2 a = sub2(f2make(__int_as_float((int)r[h & 1][2 * i] + 0x4B400000),
-                                                 __int_as_float((int)r[h & 1][2 * i + 1] + 0x4B400000)), mg);
-                        acc[8 * h + i] = fma2(a, s2, acc[8 * h + i]);
+                    for (int i = 0; i < 16; ++i) {
+                        const f2 a = f2make(__int2float_rn((int)r[2 * i]), __int2float_rn((int)r[2 * i + 1]));
+                        acc[16 * h + i] = fma2(a, s2, acc[16 * h + i]);
                     }
                 }
             }
@@ -860,16 +900,16 @@ static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, i
     return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BN, int STAGES, bool TDC = false>
+template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false>
 static dmpq_status set_pair_attrs() {
     using L = PairLayout<KIND, BN, STAGES>;
-    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC, QNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              L::TOTAL) != cudaSuccess)
         return check_launch("dmpq_gemm(smem attribute)");
     return DMPQ_OK;
 }
 
-template <int KIND, int BN, int STAGES, bool TDC = false>
+template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false>
 static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
     using L = PairLayout<KIND, BN, STAGES>;
     constexpr bool FP4 = KIND == 1;
@@ -892,10 +932,10 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     p.num_m_tiles = (p.m + 255) / 256;
     p.num_n_tiles = (p.n + BN - 1) / BN;
     p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
-    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC>;
+    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC, QNT>;
     static bool attr_set = false;   // per process and kernel (dmpq_prepare sets them ahead of graph capture)
     if (!attr_set) {
-        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES, TDC>();
+        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES, TDC, QNT>();
         if (rc != DMPQ_OK) return rc;
         attr_set = true;
     }
@@ -969,6 +1009,8 @@ extern "C" dmpq_status dmpq_prepare(void) {
     if (rc == DMPQ_OK) rc = set_pair_attrs<0, 256, 5, true>();   // fused TDC refresh variants
     if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5, true>();
     if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5, true>();
+    if (rc == DMPQ_OK) rc = set_pair_attrs<0, 256, 5, false, true>();   // producer-fused NVFP4 quantizer
+    if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5, false, true>();
     if (rc == DMPQ_OK && cudaFuncSetAttribute(dmpq_gemm_i8b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               I8BLayout::TOTAL) != cudaSuccess)
         rc = check_launch("dmpq_prepare(per-block INT8 GEMM)");
@@ -986,7 +1028,8 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
     const int m = A->m, n = W->n, k = A->k;
     DMPQ_REQUIRE(k == W->k && k > 0 && k % 64 == 0 && n > 0 && n % 32 == 0 && m >= 0, DMPQ_ESHAPE,
                  "dmpq_gemm: need A.k == W.k, k %% 64 == 0, n %% 32 == 0 (m=%d n=%d k=%d Wk=%d)", m, n, k, W->k);
-    DMPQ_REQUIRE(Y || Y32 || acc_or_null, DMPQ_EINVAL, "dmpq_gemm: no output");
+    const bool qnt = ep && (ep->flags & DMPQ_EP_QUANT_NVFP4);
+    DMPQ_REQUIRE(Y || Y32 || acc_or_null || qnt, DMPQ_EINVAL, "dmpq_gemm: no output");
     DMPQ_REQUIRE(!Y || (aligned16(Y) && ldy >= n && ldy % 8 == 0), DMPQ_EALIGN, "dmpq_gemm: Y / ldy alignment");
     DMPQ_REQUIRE(!Y32 || aligned16(Y32), DMPQ_EALIGN, "dmpq_gemm: Y32 alignment");
     DMPQ_REQUIRE(!acc_or_null || !fp4, DMPQ_EINVAL, "dmpq_gemm: raw accumulators are INT8-only");
@@ -1013,6 +1056,17 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
     }
     p.Y = Y; p.ldy = ldy; p.Y32 = Y32; p.acc_out = acc_or_null;
     if (ep) { p.run_if = ep->run_if; p.run_if_value = ep->run_if_value; }
+    if (qnt) {
+        const dmpq_act* q = ep->q_out;
+        DMPQ_REQUIRE(q && q->fmt == DMPQ_FMT_NVFP4 && q->m == m && q->k == n && n % 64 == 0, DMPQ_ESHAPE,
+                     "dmpq_gemm: DMPQ_EP_QUANT_NVFP4 needs an NVFP4 [m x n] q_out and n %% 64 == 0");
+        DMPQ_REQUIRE(q->codes && q->sf && q->g && ep->q_amax && aligned16(q->codes) && aligned16(q->sf), DMPQ_EALIGN,
+                     "dmpq_gemm: DMPQ_EP_QUANT_NVFP4 output pointers");
+        DMPQ_REQUIRE(!(p.flags & DMPQ_EP_TDC_REFRESH) && A->scale_block == 0, DMPQ_EUNSUPPORTED,
+                     "dmpq_gemm: the fused quantizer is built for the plain INT8 / NVFP4 kernels");
+        p.q_codes = reinterpret_cast<uint8_t*>(q->codes); p.q_sf = q->sf; p.q_g = q->g; p.q_amax = ep->q_amax;
+        p.q_kc4 = n / 64; p.q_m_pad = (m + 127) / 128 * 128;
+    }
     if (m == 0) {
         if (p.flags & DMPQ_EP_TDC_REFRESH) {   // empty sums
             if (cudaMemsetAsync(ep->tdc_stats, 0, 7 * sizeof(double), reinterpret_cast<cudaStream_t>(s)) != cudaSuccess)
@@ -1032,12 +1086,14 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         p.kc4 = k / 64;
         p.sfb_row_tiles = (n + 127) / 128;
         if (tdc) return launch_gemm_pair<1, 192, 5, true>(p, A->codes, W->fp4_codes, st);
+        if (qnt) return launch_gemm_pair<1, 192, 5, false, true>(p, A->codes, W->fp4_codes, st);
         if (fp4_bn() == 256) return launch_gemm_pair<1, 256, 5>(p, A->codes, W->fp4_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st)
                                  : launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
     } else if (A->fmt == DMPQ_FMT_BF16) {
         DMPQ_REQUIRE(A->codes && W->bf16_w && aligned16(A->codes) && aligned16(W->bf16_w), DMPQ_EALIGN,
                      "dmpq_gemm: BF16 path needs A->codes (bf16 activation) and W->bf16_w");
+        DMPQ_REQUIRE(!qnt, DMPQ_EUNSUPPORTED, "dmpq_gemm: the fused quantizer is built for the INT8 / NVFP4 kernels");
         p.kbytes = 2 * k;
         if (tdc) return launch_gemm_pair<2, 256, 5, true>(p, A->codes, W->bf16_w, st);
         return gemm_stages() == 5 ? launch_gemm_pair<2, 256, 5>(p, A->codes, W->bf16_w, st)
@@ -1054,6 +1110,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
             return launch_gemm_i8b(p, A->codes, W->i8_codes, st);
         }
         if (tdc) return launch_gemm_pair<0, 256, 5, true>(p, A->codes, W->i8_codes, st);
+        if (qnt) return launch_gemm_pair<0, 256, 5, false, true>(p, A->codes, W->i8_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st)
                                  : launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);
     }

@@ -284,12 +284,15 @@ def dmpq_gemm(A: QuantAct, W: PackedWeights, Y: torch.Tensor | None = None, Y32:
               residual: torch.Tensor | None = None, gate: torch.Tensor | None = None,
               tdc_x_in: torch.Tensor | None = None, tdc_delta: torch.Tensor | None = None,
               tdc_stats: torch.Tensor | None = None, tdc_workspace: torch.Tensor | None = None,
-              run_if: torch.Tensor | None = None, run_if_value: int = 0):
+              run_if: torch.Tensor | None = None, run_if_value: int = 0,
+              quant_out: QuantAct | None = None, quant_amax: torch.Tensor | None = None):
     """Y = epilogue(A @ W^T) on tcgen05 (kind::i8 or kind::mxf4nvf4). With tdc_x_in / tdc_delta /
     tdc_stats / tdc_workspace the epilogue also runs the TDC refresh of X_out = Y (fused tdc_step)."""
     flags = (L.EP_BIAS if (bias and W.bias is not None) else 0) | (L.EP_GELU_TANH if gelu else 0)
     if residual is not None:
         flags |= L.EP_RESIDUAL
+    if quant_out is not None:   # producer-fused NVFP4 quantization of bf16(Y) (P:336, NEXT-2)
+        flags |= L.EP_QUANT_NVFP4
     if tdc_x_in is not None:
         flags |= L.EP_TDC_REFRESH
         for t_, n_ in ((tdc_x_in, "tdc_x_in"), (tdc_delta, "tdc_delta")):
@@ -298,7 +301,8 @@ def dmpq_gemm(A: QuantAct, W: PackedWeights, Y: torch.Tensor | None = None, Y32:
     if flags or run_if is not None:   # run_if: int32 device flag, the GEMM runs iff *run_if == run_if_value (R18)
         ep = L.Epilogue(flags, _ptr(gate), _ptr(residual), 0 if residual is None else residual.stride(0),
                         _ptr(tdc_x_in), _ptr(tdc_delta), _ptr(tdc_stats), _ptr(tdc_workspace), _ptr(run_if),
-                        int(run_if_value))
+                        int(run_if_value), None if quant_out is None else ctypes.addressof(quant_out.c),
+                        _ptr(quant_amax))
     if Y is not None:
         _check_dev(Y, "Y", torch.bfloat16)
     L.check("dmpq_gemm", L.lib().dmpq_gemm(

@@ -53,6 +53,9 @@ MODES = {
     "hadamard_int8_cast": (True, False, 25.0, False, 0.02, False, True),
     # per-block symmetric INT8 over the Hadamard blocks (R17, NEXT-1)
     "hadamard_int8_block": (True, False, 25.0, False, 0.02, False, False, True),
+    # producer-fused NVFP4 quantization of the FFN2 input in FFN1's epilogue (NEXT-2; plain quantizer);
+    # tau_gamma scaled so that the FFN2 layer routes NVFP4 on some steps
+    "dmpq_fused_quant": (False, False, 25.0, False, 0.02, False, False, False, True),
 }
 
 
@@ -76,9 +79,11 @@ def run(request):
     fused = len(MODES[request.param]) > 5 and MODES[request.param][5]
     cast = len(MODES[request.param]) > 6 and MODES[request.param][6]
     i8b = len(MODES[request.param]) > 7 and MODES[request.param][7]
+    fq = len(MODES[request.param]) > 8 and MODES[request.param][8]
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
     stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o,
-                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused, int8_cast=cast, int8_block=i8b)
+                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused, int8_cast=cast, int8_block=i8b, fuse_quant=fq,
+                     tau_gamma=[0.05] * 6 if fq else None)
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):

@@ -733,3 +733,36 @@ def test_gemm_int8_blocks_rel_l2(D, orc, m, n, k):
     got = y32r.cpu().numpy().astype(np.float64)
     want = gate.cpu().numpy().astype(np.float64)[None, :] * yp + res.cpu().float().numpy().astype(np.float64)
     assert np.all(np.abs(got - want) <= np.abs(want) * 2.0 ** -23 + 1e-30)
+
+
+@pytest.mark.parametrize("fmt,m,n,k,gelu", [(0, 300, 512, 256, True), (1, 300, 512, 256, True), (1, 1029, 1920, 512, True),
+                                            (0, 129, 3072, 128, False), (1, 35, 768, 3072, True)])
+def test_gemm_fused_nvfp4_quant(D, orc, fmt, m, n, k, gelu):
+    """Producer-fused NVFP4 quantization in the GEMM epilogue (DMPQ_EP_QUANT_NVFP4, NEXT-2):
+    the codes, swizzled scales (padding rows zeroed) and amax it writes equal the standalone
+    quantizer's on the same GEMM's bf16 output, and the oracle's; without Y the codes are the same."""
+    x = synth.dit_activation(m, k, seed=m + 11 * k)
+    w, b = synth.linear_weight(n, k, seed=n + 13 * k)
+    pw = D.dmpq_pack_weights(w.cuda(), b)
+    g = torch.tensor([0.01], device="cuda")
+    a = D.QuantAct.empty(fmt, m, k, "cuda", g=g if fmt == 1 else None)
+    D.dmpq_quantize_act(x.cuda(), out_fp4=a if fmt == 1 else None, out_i8=a if fmt == 0 else None)
+    gq = torch.tensor([0.003], device="cuda")
+    q1 = D.QuantAct.empty(D.FMT_NVFP4, m, n, "cuda", g=gq)
+    q1.sf.fill_(0xAB)
+    am1 = torch.zeros(1, device="cuda")
+    y = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a, pw, Y=y, gelu=gelu, quant_out=q1, quant_amax=am1)
+    q2 = D.QuantAct.empty(D.FMT_NVFP4, m, n, "cuda", g=gq)
+    am2 = torch.zeros(1, device="cuda")
+    D.dmpq_quantize_act(y, out_fp4=q2, amax_out=am2)
+    q3 = D.QuantAct.empty(D.FMT_NVFP4, m, n, "cuda", g=gq)
+    am3 = torch.zeros(1, device="cuda")
+    D.dmpq_gemm(a, pw, gelu=gelu, quant_out=q3, quant_amax=am3)   # no bf16 output at all
+    torch.cuda.synchronize()
+    assert torch.equal(q1.codes, q2.codes) and torch.equal(q1.sf, q2.sf) and am1.item() == am2.item()
+    assert torch.equal(q3.codes, q1.codes) and torch.equal(q3.sf, q1.sf) and am3.item() == am1.item()
+    c, s_ = orc.nvfp4_quantize(synth.bits(y.cpu()), 0.003)
+    assert np.array_equal(q1.codes.cpu().numpy(), c)
+    assert np.array_equal(q1.sf.cpu().numpy(), orc.sf_swizzle(s_, m, n))
+    assert am1.item() == orc.amax_bf16(synth.bits(y.cpu()))
