@@ -434,300 +434,6 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
     }
 }
 
-// ============================================================================
-// Two threads per 128-element Hadamard block (the production kernel; quant_had_kernel above is
-// the one-thread-per-block original, DMPQ_QUANT_HAD1=1). Thread (block b, half h) holds the 64
-// elements of half h: FHT stages h = 1..32 run in its registers and the last stage (pairs 64
-// apart) exchanges 32 values with the partner thread (lane ^ 8) by shuffles, after which each
-// thread owns two runs of 32 consecutive outputs (32h.., 64 + 32h..) -- whole NVFP4 blocks.
-// Same arithmetic in the same order as the oracle's butterflies (R14): codes stay bit-exact.
-// Half the registers per thread (~100), so ~1.5x the resident warps of the original: the
-// kernel is latency-bound at ~9 instructions per element (ncu: 55 % issue, "wait" and
-// math-pipe stalls with 3 warps per scheduler). Lanes 0-7 / 8-15 of each 16-lane group take
-// half 0 / half 1 of eight consecutive blocks, so every quarter-warp LDS.128 reads eight
-// consecutive 128-byte lines (conflict-free under the 128-byte swizzle).
-// ============================================================================
-constexpr int HT2_MAX = 256;
-constexpr int H2_MAX_SEG = HT2_MAX / 8;
-
-template <bool LN, bool PDR, bool WH, int FMT = 0>
-__global__ void __launch_bounds__(HT2_MAX, 2) quant_had2_kernel(const QuantParams p, const __grid_constant__ CUtensorMap tmX,
-                                                                 int tpr, int R, int set_stride, int nbuf, int split) {
-    extern __shared__ uint8_t hsm_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(hsm_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t rtab = sbase + nbuf * set_stride;   // 256 fp32 block reciprocals
-    const uint32_t red = rtab + 1024;
-    const uint32_t bar0 = red + 8 * H2_MAX_SEG * 4;
-
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int grp = tid / tpr, t = tid - grp * tpr;
-    const int hh = (t >> 3) & 1, blk = (t & 7) + ((t >> 4) << 3);   // half and block of this thread
-    const int nb = p.k >> 7;
-    const bool cvalid = blk < nb;
-    const int nsets = (p.m + R - 1) / R;
-    const int iters = (int)blockIdx.x < nsets ? (nsets - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-    const uint32_t tx_bytes = (uint32_t)(R * nb * 256);
-    Seg8 sr{red, grp * (tpr >> 3), tpr >> 3};
-    sr.stride = H2_MAX_SEG;
-    const bool want_fp4 = FMT ? (FMT & 1) != 0 : p.fp4_codes != nullptr;
-    const bool want_i8 = FMT ? (FMT & 2) != 0 : p.i8_codes != nullptr;
-    const bool i8_block = FMT ? (FMT & 4) != 0 : p.i8_block != 0;
-
-    const float g = want_fp4 ? *p.g : 1.0f;
-    const bool g_ok = g >= 8.0779356e-28f && g <= 1.2379400e27f;   // [2^-90, 2^90]
-    const float a_lo = fmaxf(6.3108872e-30f, __fmul_rn(g, 6.3108872e-30f));
-    const float a_hi = fminf(FM_HI, __fmul_rn(g, 5.0706024e30f));
-    const float rg = g_ok ? recip_refined(g) : 0.0f;
-    const f2 ng2 = f2make(-g, -g), rg2 = f2make(rg, rg);
-    const f2 n6 = f2make(-6.0f, -6.0f), r6 = f2make(0.16666667163372039795f, 0.16666667163372039795f);
-    for (int s_ = tid; s_ < 256; s_ += blockDim.x) {
-        const float eff = __fmul_rn(e4m3_decode((uint32_t)s_), g);
-        hsts_f32(rtab + 4u * s_, eff > 0.0f ? __frcp_rn(eff) : 0.0f);
-    }
-    if (tid == 0) {
-        prefetch_tmap(&tmX);
-        for (int j = 0; j < nbuf; ++j) {
-            mbar_init(bar0 + 8 * j, 1);
-            mbar_init(bar0 + 8 * (nbuf + j), (blockDim.x + 31) >> 5);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-    auto issue = [&](int j, int set) {
-        const uint32_t dst = sbase + j * set_stride;
-        mbar_arrive_expect_tx(bar0 + 8 * j, tx_bytes);
-        if (split) tma_load_4d(dst, &tmX, 0, 0, 0, set * R, bar0 + 8 * j);
-        else tma_load_3d_h(dst, &tmX, 0, 0, set * R, bar0 + 8 * j);
-    };
-    if (tid == 0)
-        for (int j = 0; j < nbuf && j < iters; ++j) issue(j, (int)blockIdx.x + j * (int)gridDim.x);
-
-    const int bb0 = cvalid ? blk : 0;
-    const uint32_t line = split ? (uint32_t)(grp * 2 * nb + hh * nb + bb0) : (uint32_t)(grp * 2 * nb + 2 * bb0 + hh);
-    const uint32_t x0 = line * 128 + ((line & 7) << 4);
-
-    const float zr = hlds_f32(rtab);   // +0, opaque to ptxas (int8x4_magic)
-    const f2 z2 = f2make(zr, zr);
-    float my_amax = 0.0f, my_amax_in = 0.0f;
-    int b = 0;
-    uint32_t ph = 0;
-    for (int it = 0; it < iters; ++it) {
-        const int set = (int)blockIdx.x + it * (int)gridDim.x;
-        const int row = set * R + grp;
-        const bool row_live = row < p.m;
-        const bool live = row_live && cvalid;
-        const int s0 = (it & 1) * 4;
-        mbar_wait(bar0 + 8 * b, ph);
-        const uint32_t buf = sbase + b * set_stride;
-
-        f2 Y[32];   // this thread's 64 elements: pair q = elements (2q, 2q + 1) of its half
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const uint4 v = hlds128((buf + x0) ^ (u << 4));
-            Y[4 * u] = bf16x2_to_f2(v.x);
-            Y[4 * u + 1] = bf16x2_to_f2(v.y);
-            Y[4 * u + 2] = bf16x2_to_f2(v.z);
-            Y[4 * u + 3] = bf16x2_to_f2(v.w);
-        }
-
-        if constexpr (LN) {
-            f2 s1 = f2make(0.0f, 0.0f), s2 = f2make(0.0f, 0.0f);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                s1 = add2(s1, Y[q]);
-                s2 = fma2(Y[q], Y[q], s2);
-            }
-            float S1 = cvalid ? __fadd_rn(f2lo(s1), f2hi(s1)) : 0.0f, S2 = cvalid ? __fadd_rn(f2lo(s2), f2hi(s2)) : 0.0f;
-            sr.sum2(S1, S2, s0 + 0);
-            const float mean = __fdiv_rn(S1, (float)p.k);
-            const float var = fmaxf(__fsub_rn(__fdiv_rn(S2, (float)p.k), __fmul_rn(mean, mean)), 0.0f);
-            const float rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, p.ln_eps)));
-            const f2 rs = f2make(rstd, rstd), nmr = f2make(-__fmul_rn(mean, rstd), -__fmul_rn(mean, rstd));
-            const f2 pm = f2make(1.0f, -1.0f);
-            f2 sa = f2make(0.0f, 0.0f);
-            float mx = 0.0f;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                float hv[8];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int q = 4 * u + j;
-                    const f2 v = fma2(Y[q], rs, nmr);
-                    const float a = __uint_as_float(pack_bf16x2(0.0f, f2lo(v))), bv = __uint_as_float(pack_bf16x2(0.0f, f2hi(v)));
-                    hv[2 * j] = a;
-                    hv[2 * j + 1] = bv;
-                    if constexpr (PDR) {
-                        const f2 ab = habs2(f2make(a, bv));
-                        sa = add2(sa, ab);
-                        mx = fmaxf(mx, fmaxf(f2lo(ab), f2hi(ab)));
-                    }
-                    Y[q] = fma2(f2make(bv, bv), pm, f2make(a, a));
-                }
-                if (WH && live) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        w[j] = __byte_perm(__float_as_uint(hv[2 * j]), __float_as_uint(hv[2 * j + 1]), 0x7632);
-                    *reinterpret_cast<uint4*>(p.h_out + (size_t)row * p.ldh + (size_t)blk * 128 + hh * 64 + u * 8) =
-                        make_uint4(w[0], w[1], w[2], w[3]);
-                }
-            }
-            if constexpr (PDR) {
-                my_amax_in = fmaxf(my_amax_in, cvalid ? mx : 0.0f);
-                const float rsum = sr.sum(cvalid ? __fadd_rn(f2lo(sa), f2hi(sa)) : 0.0f, s0 + 3);
-                if (t == 0 && row_live && p.row_abs_sum) p.row_abs_sum[row] = rsum;
-            }
-        } else {
-            if constexpr (PDR) {
-                f2 sa = f2make(0.0f, 0.0f);
-                float mx = 0.0f;
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const f2 a = habs2(Y[q]);
-                    sa = add2(sa, a);
-                    mx = fmaxf(mx, fmaxf(f2lo(a), f2hi(a)));
-                }
-                my_amax_in = fmaxf(my_amax_in, cvalid ? mx : 0.0f);
-                const float rsum = sr.sum(cvalid ? __fadd_rn(f2lo(sa), f2hi(sa)) : 0.0f, s0 + 3);
-                if (t == 0 && row_live && p.row_abs_sum) p.row_abs_sum[row] = rsum;
-            }
-            const f2 pm = f2make(1.0f, -1.0f);
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const float a = f2lo(Y[q]), bv = f2hi(Y[q]);
-                Y[q] = fma2(f2make(bv, bv), pm, f2make(a, a));
-            }
-        }
-
-        // FHT stages 2..32 inside the thread's half (R14)
-#pragma unroll
-        for (int hp = 1; hp < 32; hp <<= 1) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                if (q & hp) continue;
-                const f2 a = Y[q], bv = Y[q + hp];
-                Y[q] = add2(a, bv);
-                Y[q + hp] = sub2(a, bv);
-            }
-        }
-
-        // the row set is in registers: release buffer b (see quant_had_kernel)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
-        if (tid == 0 && it + nbuf < iters) {
-            mbar_wait(bar0 + 8 * (nbuf + b), ph);
-            issue(b, set + nbuf * (int)gridDim.x);
-        }
-
-        // FHT stage 64 across the pair of threads: out[i] = fl(a[i] + a[i+64]), out[i+64] = fl(a[i] - a[i+64]);
-        // half 0 keeps i in [0, 32), half 1 keeps i in [32, 64)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const f2 snd = hh ? Y[j] : Y[16 + j];
-            const f2 rcv = f2make(__shfl_xor_sync(0xffffffffu, f2lo(snd), 8), __shfl_xor_sync(0xffffffffu, f2hi(snd), 8));
-            const f2 a = hh ? rcv : Y[j];
-            const f2 bv = hh ? Y[16 + j] : rcv;
-            Y[j] = add2(a, bv);
-            Y[16 + j] = sub2(a, bv);
-        }
-        // Y[0..15] = outputs 32h .. 32h+31 (run A), Y[16..31] = outputs 64+32h .. (run B)
-
-        float a[4];   // |y| maxima of this thread's four 16-element blocks
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = habsmax8p(&Y[8 * i]);
-        const float tmax = cvalid ? hmax3(a[0], a[1], fmaxf(a[2], a[3])) : 0.0f;
-        my_amax = fmaxf(my_amax, tmax);
-
-        if (want_fp4 && live) {
-            const float lo = fminf(fminf(a[0], a[1]), fminf(a[2], a[3]));
-            uint32_t s[2];   // E4M3 codes of the run's two blocks in bytes 0, 1
-            if (g_ok && lo >= a_lo && tmax <= a_hi) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    s[j] = e4m3x2(div2_fast(div2_fast(f2make(a[2 * j], a[2 * j + 1]), n6, r6), ng2, rg2));
-            } else {
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    s[j] = e4m3_rn_satfinite(__fdiv_rn(__fdiv_rn(a[2 * j], 6.0f), g)) |
-                           (e4m3_rn_satfinite(__fdiv_rn(__fdiv_rn(a[2 * j + 1], 6.0f), g)) << 8);
-            }
-            uint8_t* cbase = p.fp4_codes + (size_t)row * (p.k >> 1) + (size_t)blk * 64 + hh * 16;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {   // run j: 32 codes -> one 16-byte store
-                uint32_t c[4];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const float r = rtab_lookup(rtab + 4u * ((s[j] >> (8 * e)) & 0xFFu));
-                    const f2 r2 = f2make(r, r);
-                    const f2* y = &Y[16 * j + 8 * e];
-                    c[2 * e] = e2m1x8(mul2(y[0], r2), mul2(y[1], r2), mul2(y[2], r2), mul2(y[3], r2));
-                    c[2 * e + 1] = e2m1x8(mul2(y[4], r2), mul2(y[5], r2), mul2(y[6], r2), mul2(y[7], r2));
-                }
-                *reinterpret_cast<uint4*>(cbase + 32 * j) = make_uint4(c[0], c[1], c[2], c[3]);
-            }
-            uint8_t* sp = sf_row_ptr(p.fp4_sf, p.kc4, row) + (size_t)blk * 1024 + 2 * hh;
-            *reinterpret_cast<uint16_t*>(sp) = (uint16_t)s[0];
-            *reinterpret_cast<uint16_t*>(sp + 512) = (uint16_t)s[1];
-        }
-        if (want_i8) {
-            // per token: the row maximum; per block (R17): the maximum over both halves of the block
-            const float bmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-            const float am = i8_block ? bmax : sr.max(tmax, s0 + 2);
-            const float rcp = am > 0.0f ? __fdiv_rn(127.0f, am) : 0.0f;
-            if (i8_block) {
-                if (live && hh == 0) p.i8_scale[(size_t)row * nb + blk] = am > 0.0f ? __fdiv_rn(am, 127.0f) : 1.0f;
-            } else if (t == 0 && row_live) {
-                p.i8_scale[row] = am > 0.0f ? __fdiv_rn(am, 127.0f) : 1.0f;
-            }
-            if (live) {
-                const f2 r2 = f2make(rcp, rcp);
-                int8_t* ob = p.i8_codes + (size_t)row * p.k + (size_t)blk * 128 + hh * 32;
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {   // run j: 32 codes -> two 16-byte stores
-                    uint4* op = reinterpret_cast<uint4*>(ob + 64 * j);
-#pragma unroll
-                    for (int v = 0; v < 2; ++v) {
-                        const f2* y = &Y[16 * j + 8 * v];
-                        op[v] = make_uint4(int8x4_magic(y[0], y[1], r2, z2), int8x4_magic(y[2], y[3], r2, z2),
-                                           int8x4_magic(y[4], y[5], r2, z2), int8x4_magic(y[6], y[7], r2, z2));
-                    }
-                }
-            }
-        }
-        if (++b == nbuf) {
-            b = 0;
-            ph ^= 1u;
-        }
-    }
-    if (want_fp4) {
-        const int pad_rows = p.m_pad - p.m;
-        for (int idx = blockIdx.x * blockDim.x + tid; idx < pad_rows * p.kc4; idx += gridDim.x * blockDim.x) {
-            const int r = p.m + idx / p.kc4, c4 = idx % p.kc4;
-            *reinterpret_cast<uint32_t*>(sf_row_ptr(p.fp4_sf, p.kc4, r) + (size_t)c4 * 512) = 0u;
-        }
-    }
-    if (p.amax_out || p.amax_in) {
-        const float am = warp_max(my_amax), ai = warp_max(my_amax_in);
-        const int nw = (int)(blockDim.x + 31) >> 5;
-        __syncthreads();
-        if (lane == 0) {
-            hsts_f32(red + 4u * (tid >> 5), am);
-            hsts_f32(red + 4u * (H2_MAX_SEG + (tid >> 5)), ai);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            float m0 = 0.0f, m1 = 0.0f;
-            for (int w = 0; w < nw; ++w) {
-                m0 = fmaxf(m0, hlds_f32(red + 4u * w));
-                m1 = fmaxf(m1, hlds_f32(red + 4u * (H2_MAX_SEG + w)));
-            }
-            if (p.amax_out) atomic_max_nonneg(p.amax_out, m0);
-            if (p.amax_in) atomic_max_nonneg(p.amax_in, m1);
-        }
-    }
-}
-
 // 4-D view of X: {64 elements, nb blocks (256 B), 2 halves (128 B), m rows}, box {64, nb, 2, R}:
 // a row lands in shared memory as [half][block][64 elements]. 128-byte swizzle.
 bool make_tmap_had_split(CUtensorMap* tm, const void* base, int m, int nb, int ldx, int R) {
@@ -782,17 +488,7 @@ dmpq_status prepare_quant_had() {
                              (const void*)quant_had_kernel<false, false, false>,    (const void*)quant_had_kernel<true, false, false>,
                              (const void*)quant_had_kernel<false, false, false, 6>, (const void*)quant_had_kernel<false, false, false, 7>,
                              (const void*)quant_had_kernel<true, false, false, 6>,  (const void*)quant_had_kernel<true, false, false, 7>};
-    const void* kernels2[] = {(const void*)quant_had2_kernel<false, false, false, 1>, (const void*)quant_had2_kernel<false, false, false, 2>,
-                              (const void*)quant_had2_kernel<false, false, false, 3>, (const void*)quant_had2_kernel<true, false, false, 1>,
-                              (const void*)quant_had2_kernel<true, false, false, 2>,  (const void*)quant_had2_kernel<true, false, false, 3>,
-                              (const void*)quant_had2_kernel<true, false, true>,      (const void*)quant_had2_kernel<false, true, false>,
-                              (const void*)quant_had2_kernel<true, true, false>,      (const void*)quant_had2_kernel<true, true, true>,
-                              (const void*)quant_had2_kernel<false, false, false>,    (const void*)quant_had2_kernel<true, false, false>,
-                              (const void*)quant_had2_kernel<false, false, false, 6>, (const void*)quant_had2_kernel<false, false, false, 7>,
-                              (const void*)quant_had2_kernel<true, false, false, 6>,  (const void*)quant_had2_kernel<true, false, false, 7>};
     bool ok = true;
-    for (const void* k : kernels2)
-        ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) == cudaSuccess;
     for (const void* k : kernels)
         ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, H_MAX_SMEM) == cudaSuccess;
     if (!ok)
@@ -800,76 +496,11 @@ dmpq_status prepare_quant_had() {
     return DMPQ_OK;
 }
 
-static int had2_ctas_per_sm(int threads, int smem) {
-    static std::mutex mu;
-    static int cache_threads[8] = {0}, cache_smem[8] = {0}, cache_n[8] = {0};
-    std::lock_guard<std::mutex> lk(mu);
-    for (int i = 0; i < 8; ++i)
-        if (cache_threads[i] == threads && cache_smem[i] == smem) return cache_n[i];
-    int n = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quant_had2_kernel<false, false, false>, threads, smem) != cudaSuccess || n < 1) {
-        cudaGetLastError();
-        n = 1;
-    }
-    for (int i = 0; i < 8; ++i)
-        if (cache_threads[i] == 0) { cache_threads[i] = threads; cache_smem[i] = smem; cache_n[i] = n; break; }
-    return n;
-}
-
-static dmpq_status launch_quant_had2(const QuantParams& p, cudaStream_t s) {
-    const int nb = p.k / 128;
-    int tpr = (2 * nb + 15) / 16 * 16;
-    if (tpr > 32) tpr = (tpr + 31) / 32 * 32;
-    int R = 1;
-    while ((R * tpr) % 32) ++R;
-    while (R * tpr < 96) R *= 2;
-    const int threads = R * tpr;
-    const int set_bytes = R * nb * 256;
-    const int set_stride = (set_bytes + 1023) / 1024 * 1024;
-    int nbuf = 2;
-    while (nbuf < 4 && nbuf * set_stride < 32 * 1024) ++nbuf;
-    const int smem = nbuf * set_stride + 1024 + 8 * H2_MAX_SEG * 4 + 16 * nbuf + 1024;
-    if (threads > HT2_MAX || smem > H_MAX_SMEM)
-        return set_error(DMPQ_ESHAPE, "dmpq_quantize_act: k=%d exceeds the Hadamard quantizer's limits", p.k);
-    CUtensorMap tm;
-    int split = 1;
-    if (!make_tmap_had_split(&tm, p.X, p.m, nb, p.ldx, R)) {
-        split = 0;
-        if (!make_tmap_had_lines(&tm, p.X, p.m, nb, p.ldx, R))
-            return set_error(DMPQ_ECUDA, "dmpq_quantize_act: cuTensorMapEncodeTiled failed");
-    }
-    const int nsets = (p.m + R - 1) / R;
-    const int grid = std::max(1, std::min(nsets, had2_ctas_per_sm(threads, smem) * num_sms()));
-    const bool ln = (p.flags & DMPQ_QF_LAYERNORM) != 0, pdr = p.row_abs_sum != nullptr || p.amax_in != nullptr;
-    const bool wh = ln && (p.flags & DMPQ_QF_WRITE_H) != 0;
-#define DMPQ_HAD2(a, b, c) quant_had2_kernel<a, b, c><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split)
-#define DMPQ_HAD2_F(a, f) quant_had2_kernel<a, false, false, f><<<grid, threads, smem, s>>>(p, tm, tpr, R, set_stride, nbuf, split)
-    if (ln && pdr) { if (wh) DMPQ_HAD2(true, true, true); else DMPQ_HAD2(true, true, false); }
-    else if (pdr) DMPQ_HAD2(false, true, false);
-    else if (ln && wh) DMPQ_HAD2(true, false, true);
-    else {
-        const int f = (p.fp4_codes ? 1 : 0) | (p.i8_codes ? 2 : 0) | (p.i8_codes && p.i8_block ? 4 : 0);
-        if (ln) {
-            if (f == 1) DMPQ_HAD2_F(true, 1); else if (f == 2) DMPQ_HAD2_F(true, 2); else if (f == 3) DMPQ_HAD2_F(true, 3);
-            else if (f == 6) DMPQ_HAD2_F(true, 6); else if (f == 7) DMPQ_HAD2_F(true, 7); else DMPQ_HAD2(true, false, false);
-        } else {
-            if (f == 1) DMPQ_HAD2_F(false, 1); else if (f == 2) DMPQ_HAD2_F(false, 2); else if (f == 3) DMPQ_HAD2_F(false, 3);
-            else if (f == 6) DMPQ_HAD2_F(false, 6); else if (f == 7) DMPQ_HAD2_F(false, 7); else DMPQ_HAD2(false, false, false);
-        }
-    }
-#undef DMPQ_HAD2
-#undef DMPQ_HAD2_F
-    return check_launch("dmpq_quantize_act");
-}
-
 dmpq_status launch_quant_had(const QuantParams& p, cudaStream_t s) {
     static std::once_flag once;
     static dmpq_status prep = DMPQ_OK;
     std::call_once(once, [] { prep = prepare_quant_had(); });
     if (prep != DMPQ_OK) return prep;
-    // DMPQ_QUANT_HAD1=1: the one-thread-per-block kernel (A/B measurements)
-    static const bool had1 = [] { const char* e = getenv("DMPQ_QUANT_HAD1"); return e && e[0] == '1'; }();
-    if (!had1) return launch_quant_had2(p, s);
     const int nb = p.k / 128;
     int tpr = (nb + 7) / 8 * 8;
     if (tpr > 32) tpr = (tpr + 31) / 32 * 32;
