@@ -56,5 +56,35 @@ for fmt in (D.FMT_INT8, D.FMT_NVFP4):
                         hadamard=True)
     D.dmpq_gemm(a, pw2, Y=y2, residual=res, gate=gate)
     D.dmpq_gemm(a, pw2, Y=y2, residual=res, gate=gate, tdc_x_in=xin2, tdc_delta=d2, tdc_stats=st, tdc_workspace=wsg)
+# round 2: on-the-fly INT8 weight cast, per-block INT8 (quantizer + promotion GEMM), device PDR gate with
+# predicated GEMMs, producer-fused NVFP4 quantizer epilogue (both GEMM kinds)
+m3, k3, n3 = 300, 1920, 384
+x3 = synth.dit_activation(m3, k3, seed=9).to(dev)
+w3, b3 = synth.linear_weight(n3, k3, seed=10)
+lean = D.dmpq_pack_weights(w3.to(dev), b3.to(dev), hadamard=True, int8_resident=False, keep_bf16=True)
+scratch = torch.empty(n3 * k3, dtype=torch.int8, device=dev)
+cast = D.dmpq_cast_int8(lean, scratch)
+ab = D.QuantAct.empty(D.FMT_INT8, m3, k3, dev, scale_block=128)
+rs3 = torch.zeros(m3, device=dev)
+ai3 = torch.zeros(1, device=dev)
+D.dmpq_quantize_act(x3, out_i8=ab, hadamard=True, row_abs_sum=rs3, amax_in=ai3)
+y3 = torch.empty(m3, n3, dtype=torch.bfloat16, device=dev)
+res3 = synth.dit_activation(m3, n3, seed=11).to(dev)
+gate3 = torch.full((n3,), 0.01, device=dev)
+D.dmpq_gemm(ab, cast, Y=y3, gelu=True)
+D.dmpq_gemm(ab, cast, Y=y3, residual=res3, gate=gate3)
+flag = torch.zeros(1, dtype=torch.int32, device=dev)
+D.dmpq_outlier_gate(rs3, ai3, m3 * k3, 25.0, flag)
+a83 = D.QuantAct.empty(D.FMT_INT8, m3, k3, dev)
+D.dmpq_quantize_act(x3, out_i8=a83, hadamard=True)
+D.dmpq_gemm(a83, cast, Y=y3, run_if=flag, run_if_value=0)
+D.dmpq_gemm(D.QuantAct.bf16(x3), cast, Y=y3, run_if=flag, run_if_value=1)
+q = D.QuantAct.empty(D.FMT_NVFP4, m3, n3, dev, g=torch.tensor([0.01], device=dev))
+qa = torch.zeros(1, device=dev)
+for fmt in (D.FMT_INT8, D.FMT_NVFP4):
+    a = D.QuantAct.empty(fmt, m3, k3, dev, g=torch.tensor([0.01], device=dev) if fmt == D.FMT_NVFP4 else None)
+    D.dmpq_quantize_act(x3, out_fp4=a if fmt == D.FMT_NVFP4 else None, out_i8=a if fmt == D.FMT_INT8 else None,
+                        hadamard=True)
+    D.dmpq_gemm(a, cast, gelu=True, quant_out=q, quant_amax=qa)
 torch.cuda.synchronize()
 print("sanitize_small ok")
