@@ -92,6 +92,9 @@ constexpr int EPI_WARPS = DMPQ_EPI_WARPS;   // epilogue warps per CTA (2 per TME
 #ifndef DMPQ_GEMM_PREFETCH
 #define DMPQ_GEMM_PREFETCH 0   // L2 prefetch of the next tile's A / B rows at the start of each tile (measured 25-30 % slower)
 #endif
+#ifndef DMPQ_MAX_STAGING
+#define DMPQ_MAX_STAGING 3     // output/residual staging buffers per epilogue warp (at most)
+#endif
 #ifndef DMPQ_GEMM_RASTER
 #define DMPQ_GEMM_RASTER 0     // 0: pair c takes tiles c, c + P, ... (n-fastest); 1: a contiguous run of tiles per pair
 #endif
@@ -119,8 +122,12 @@ struct PairLayout {
     static constexpr int VEC_BYTES = 2 * 3 * BN * 4;              // [acc parity][bias|wscale|gate][BN]
     static constexpr int SMEM_LIMIT = 232448;                     // 227 KB opt-in per CTA
     // double-buffered output staging when it fits next to the stage ring, else single-buffered
+    // output / residual staging buffers per epilogue warp: 3 when they fit next to the stage ring
+    // (NVFP4 BN = 192: a warp's three chunks of a tile all get their residual requested before the
+    // accumulator is ready), else 2, else 1
     static constexpr int STAGING_BUFS =
-        (STAGING_OFFSET + EPI_WARPS * 2 * 2048 + VEC_BYTES + 512 + 1024 <= SMEM_LIMIT) ? 2 : 1;
+        (DMPQ_MAX_STAGING >= 3 && STAGING_OFFSET + EPI_WARPS * 3 * 2048 + VEC_BYTES + 512 + 1024 <= SMEM_LIMIT) ? 3
+        : (STAGING_OFFSET + EPI_WARPS * 2 * 2048 + VEC_BYTES + 512 + 1024 <= SMEM_LIMIT) ? 2 : 1;
     static constexpr int STAGING_BYTES = EPI_WARPS * STAGING_BUFS * 2048;
     static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
     static constexpr int BAR_OFFSET = VEC_OFFSET + VEC_BYTES;
@@ -149,7 +156,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     const uint32_t bar_tfull = bar_empty + STAGES * 8;
     const uint32_t bar_tempty = bar_tfull + 2 * 8;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFFSET + 2 * STAGES * 8 + 4 * 8);
-    const uint32_t bar_res = bar_full + 2 * STAGES * 8 + 4 * 8 + 16;   // [EPI_WARPS][2] residual-chunk TMA loads
+    const uint32_t bar_res = bar_full + 2 * STAGES * 8 + 4 * 8 + 16;   // [EPI_WARPS][3] residual-chunk TMA loads
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -176,7 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             mbar_init(bar_tfull + 8 * a, 1);
             mbar_init(bar_tempty + 8 * a, 2 * EPI_WARPS);  // every epilogue warp of both CTAs
         }
-        for (int i = 0; i < 2 * EPI_WARPS; ++i) mbar_init(bar_res + 8 * i, 1);
+        for (int i = 0; i < 3 * EPI_WARPS; ++i) mbar_init(bar_res + 8 * i, 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_pair(smem_u32(tmem_holder), TMEM_COLS);
@@ -197,7 +204,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int m0 = mt * 256 + (int)rank * BM;
             const int nb0 = nt * BN + (int)rank * (BN / 2);
-            if (DMPQ_GEMM_PREFETCH && tile + tstep < ts1) {
+            // next tile's A rows, one K block per K block of this tile (mode 2)
+            const bool pf2 = DMPQ_GEMM_PREFETCH == 2 && tile + tstep < ts1;
+            const int pf_m = pf2 ? ((tile + tstep) / p.num_n_tiles) * 256 + (int)rank * BM : 0;
+            if (DMPQ_GEMM_PREFETCH == 1 && tile + tstep < ts1) {
                 // the next tile's A and B rows -> L2 a whole tile ahead: at short K the stage ring
                 // (~1 us deep) cannot hide a DRAM miss at every tile start (ncu: the MMA warp waited
                 // on the full barrier ~35 % of its time at K = 3072)
@@ -220,6 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     const uint32_t sB = sA + L::A_BYTES;
                     tma_load_2d_pair(sA, &tmA, kb * BK_BYTES, m0, full_l);
                     tma_load_2d_pair(sB, &tmB, kb * BK_BYTES, nb0, full_l);
+                    if (pf2 && pf_m != m0) tma_prefetch_2d(&tmA, kb * BK_BYTES, pf_m);
                     if constexpr (FP4) {
                         const uint32_t sSFA = sB + L::B_BYTES;
                         const uint32_t sSFB = sSFA + L::SFA_BYTES;
@@ -373,9 +384,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             const uint32_t ctr0 = chunk_ctr;   // this tile's first chunk counter
             auto res_load = [&](int j) {
                 const uint32_t cj = ctr0 + (uint32_t)j;
-                mbar_arrive_expect_tx(bar_res + 8 * (ew * 2 + (int)(cj % NSB)), 2048);
+                mbar_arrive_expect_tx(bar_res + 8 * (ew * 3 + (int)(cj % NSB)), 2048);
                 tma_load_2d(staging + (cj % NSB) * 2048, &tmR, n0 + (chalf + j * CSTEP) * 32, rowbase,
-                            bar_res + 8 * (ew * 2 + (int)(cj % NSB)));
+                            bar_res + 8 * (ew * 3 + (int)(cj % NSB)));
             };
             if (tma_res && nmine > 0) {
                 if (lane == 0) {
@@ -394,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             for (int c = chalf; c < nch_here; c += CSTEP) {
                 const int jc = (c - chalf) / CSTEP;   // this warp's chunk index in the tile
                 const uint32_t buf = staging + (chunk_ctr % NSB) * 2048;
-                const uint32_t rbar = bar_res + 8 * (ew * 2 + (int)(chunk_ctr % NSB));
+                const uint32_t rbar = bar_res + 8 * (ew * 3 + (int)(chunk_ctr % NSB));
                 const uint32_t rphase = (chunk_ctr / NSB) & 1;
                 // gated-residual chunk (TMA-staged: requested ahead, see res_load; else loaded
                 // here, before the TMEM read so the two latencies overlap)
@@ -521,7 +532,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                 if (p.Y) {
                     if (!tma_res) {
                         if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
-                            if constexpr (L::STAGING_BUFS == 2) bulk_wait_read1();
+                            if constexpr (L::STAGING_BUFS == 3) bulk_wait_read2();
+                            else if constexpr (L::STAGING_BUFS == 2) bulk_wait_read1();
                             else bulk_wait_read0();
                         }
                         __syncwarp();

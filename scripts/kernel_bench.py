@@ -33,7 +33,7 @@ def timeit(fn, iters=20, warmup=3):
     return s.elapsed_time(e) / iters * 1e-3
 
 
-def bench_gemm(m, n, k, fmt, nbuf=2, block=0):
+def bench_gemm(m, n, k, fmt, nbuf=2, block=0, res=False):
     x = synth.dit_activation(m, k, seed=1).cuda()
     w, b = synth.linear_weight(n, k, seed=2)
     pw = D.dmpq_pack_weights(w.cuda(), b, hadamard=bool(block))
@@ -47,16 +47,20 @@ def bench_gemm(m, n, k, fmt, nbuf=2, block=0):
             D.dmpq_quantize_act(x, out_i8=a, hadamard=bool(block))
         acts.append(a)
     ys = [torch.empty(m, n, dtype=torch.bfloat16, device="cuda") for _ in range(nbuf)]
+    kw = {}
+    if res:   # gated residual epilogue (the O projection / FFN2 shape of the block)
+        kw = dict(residual=synth.dit_activation(m, n, seed=3).cuda(), gate=torch.full((n,), 0.01, device="cuda"))
     it = [0]
 
     def run():
         i = it[0] % nbuf
         it[0] += 1
-        D.dmpq_gemm(acts[i], pw, Y=ys[i])
+        D.dmpq_gemm(acts[i], pw, Y=ys[i], **kw)
     t = timeit(run)
     flops = 2.0 * m * n * k
     peak = PEAKS["bf16_tflops"] * (4 if fmt == D.FMT_NVFP4 else 2)
-    return dict(kernel="gemm_" + ("nvfp4" if fmt == D.FMT_NVFP4 else "int8") + ("_block" if block else ""), m=m, n=n, k=k,
+    return dict(kernel="gemm_" + ("nvfp4" if fmt == D.FMT_NVFP4 else "int8") + ("_block" if block else "") + ("_res" if res else ""),
+                m=m, n=n, k=k,
                 us=t * 1e6,
                 tflops=flops / t / 1e12, frac=flops / t / 1e12 / peak)
 
@@ -112,6 +116,7 @@ def main():
     ap.add_argument("--tdc", action="store_true")
     ap.add_argument("--shapes", default="c2,c4")
     ap.add_argument("--block", action="store_true", help="also the per-block INT8 GEMM (R17)")
+    ap.add_argument("--res", action="store_true", help="also the gated-residual epilogue at the N = 3072 shapes")
     ap.add_argument("--one", default=None, help="fmt:m,n,k  e.g. nvfp4:35552,3072,3072 (one GEMM, 5 launches)")
     a = ap.parse_args()
     if a.one:
@@ -137,6 +142,10 @@ def main():
                 r = bench_gemm(m, n, k, fmt, block=blk)
                 print(json.dumps(r), flush=True)
                 res.append(r)
+                if a.res and m == 35552 and n == 3072 and not blk:
+                    r = bench_gemm(m, n, k, fmt, res=True)
+                    print(json.dumps(r), flush=True)
+                    res.append(r)
     if a.quant:
         for (m, k) in [(35552, 3072), (35552, 12288), (65536, 1920)]:
             for fmt in (D.FMT_NVFP4, D.FMT_INT8):

@@ -10,10 +10,14 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 RUN = sys.argv[1] if len(sys.argv) > 1 else "round1"
 SRC = os.path.join(ROOT, "gpurun_out")
-DST = os.path.join(ROOT, "profiles", RUN)
+# optional second argument: output directory (on the GPU box: a gpurun_out/ subdirectory, so the
+# summaries travel back without the large .ncu-rep files)
+DST = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", RUN)
 os.makedirs(DST, exist_ok=True)
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__m_xbar2l1tex_read_bytes.sum",
@@ -65,7 +69,8 @@ if os.path.exists(lst):
             agg[name][1] += v
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(DST, "launches_by_kernel.txt"), "w") as f:
-        f.write("ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3\n")
+        f.write("ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3 "
+                "--no-cpu-baseline --no-graphs\n")
         f.write("(cold-cache, serialised launches: compare shares, not absolute times)\n\n")
         for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"{k[:80]:80s} launches={v[0]:5d} total_us={v[1]:11.1f} share={v[1] / tot:.3f}\n")
