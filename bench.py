@@ -458,7 +458,8 @@ def run_ours(args):
 
     model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
                      pdr={None: False, "delayed": True, "current": "current"}[args.pdr], m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh,
-                     int8_cast=args.int8_cast, int8_block=args.int8_block, fuse_quant=args.fuse_quant)
+                     int8_cast=args.int8_cast, int8_block=args.int8_block, fuse_quant=args.fuse_quant,
+                     overlap_refresh=args.overlap_refresh)
     # block-0 input trajectory basis: ONE seeded global [M x H] input, of which this rank takes its
     # contiguous row shard -- every world size solves the same problem (same mix, same decisions)
     A, B = synth.trajectory_basis(M, H, seed=1000 + args.seed, device=dev)
@@ -681,6 +682,7 @@ def run_ours(args):
                    "input": "one seeded global input; each rank takes its contiguous row shard", "l2": "inputs larger than L2 (multi-GB working set per step)",
                    "cuda_graphs": not args.no_graphs, "tdc_refresh": "fused in the FFN2 GEMM epilogue" if model.fuse_refresh else "own kernel",
                    "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr or False, "int8_weight_cast": args.int8_cast, "producer_fused_quant": model.fuse_quant,
+                   "tdc_refresh_overlap": model.overlap_refresh,
                    "int8_granularity": "per 128-block (R17)" if args.int8_block else "per token (R2)",
                    "delta_cache": {"format": "nvfp4" if args.cache_nvfp4 else "bf16",
                                    "bytes_per_rank": sum(d.nbytes() if args.cache_nvfp4 else d.numel() * 2
@@ -751,6 +753,8 @@ def main():
                     "instead of its own kernel (SURVEY NEXT-2; measured slower, DESIGN.md 5.7c)")
     ap.add_argument("--int8-block", action="store_true", help="per-block symmetric INT8 activations over the 128-element "
                     "Hadamard blocks (P:187, R17, NEXT-1) instead of per-token INT8")
+    ap.add_argument("--overlap-refresh", action="store_true", help="run each block's TDC refresh on a side stream "
+                    "overlapped with the next block (measured no faster; DESIGN.md 5.4)")
     ap.add_argument("--fuse-quant", action="store_true", help="producer-fused NVFP4 quantization of the FFN2 input in "
                     "FFN1's epilogue (P:336, NEXT-2; plain quantizer only, i.e. with --no-hadamard)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")

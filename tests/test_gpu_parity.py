@@ -566,19 +566,20 @@ def test_quantize_hadamard_layernorm_no_h(D, orc, k, which):
         assert np.array_equal(a4.codes.cpu().numpy(), c4)
 
 
-@pytest.mark.parametrize("had", [True, False])
-def test_graph_replay_equals_eager(D, had):
+@pytest.mark.parametrize("had,overlap", [(True, False), (False, False), (True, True)])
+def test_graph_replay_equals_eager(D, had, overlap):
     """The bench's headline pass replays one CUDA graph per (block, decision, formats) pattern.
     Six timesteps of a two-block stack replayed from graphs equal the same steps launched eagerly
-    bit for bit: outputs of every step, delta caches, FP64 statistics, global scales, decisions."""
+    bit for bit: outputs of every step, delta caches, FP64 statistics, global scales, decisions;
+    also with each block's TDC refresh overlapped with the next block on a side stream."""
     from paper_2603_18742_b200.block import DiTStack
     M, H, F, T = 1000, 128, 512, 6
     A, B = synth.trajectory_basis(M, H, seed=5)
     xs = [synth.trajectory_input(A, B, t, 50).cuda() for t in range(T)]
     runs = []
     for graphs in (False, True):
-        stack = DiTStack(2, H, F, M, "cuda", seed=4, gate_scales=[0.008, 0.012], hadamard=had,
-                         tdc_cfg=(0.001, 0.02, 2))
+        stack = DiTStack(3 if overlap else 2, H, F, M, "cuda", seed=4, gate_scales=[0.008, 0.012, 0.006][:3 if overlap else 2],
+                         hadamard=had, tdc_cfg=(0.001, 0.02, 2), overlap_refresh=overlap)
         stack.use_graphs = graphs
         outs, stats = [], []
         for t in range(T):
