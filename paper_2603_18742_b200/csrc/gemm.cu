@@ -92,9 +92,6 @@ constexpr int EPI_WARPS = DMPQ_EPI_WARPS;   // epilogue warps per CTA (2 per TME
 #ifndef DMPQ_GEMM_PREFETCH
 #define DMPQ_GEMM_PREFETCH 0   // L2 prefetch of the next tile's A / B rows at the start of each tile (measured 25-30 % slower)
 #endif
-#ifndef DMPQ_GEMM_L2HINT
-#define DMPQ_GEMM_L2HINT 0     // 1: output stores evict_first; 2: + weight (B) loads evict_last
-#endif
 #ifndef DMPQ_MAX_STAGING
 #define DMPQ_MAX_STAGING 3     // output/residual staging buffers per epilogue warp (at most)
 #endif
@@ -232,8 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     const uint32_t sA = sbase + stage * L::STAGE_BYTES;
                     const uint32_t sB = sA + L::A_BYTES;
                     tma_load_2d_pair(sA, &tmA, kb * BK_BYTES, m0, full_l);
-                    if (DMPQ_GEMM_L2HINT >= 2) tma_load_2d_pair_hint(sB, &tmB, kb * BK_BYTES, nb0, full_l, l2_policy_evict_last());
-                    else tma_load_2d_pair(sB, &tmB, kb * BK_BYTES, nb0, full_l);
+                    tma_load_2d_pair(sB, &tmB, kb * BK_BYTES, nb0, full_l);
                     if (pf2 && pf_m != m0) tma_prefetch_2d(&tmA, kb * BK_BYTES, pf_m);
                     if constexpr (FP4) {
                         const uint32_t sSFA = sB + L::B_BYTES;
@@ -401,12 +397,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             }
             mbar_wait(bar_tfull + 8 * acc, acc_phase);
             tc_fence_after();
-#ifdef DMPQ_EPI_NOOP   // development: release the accumulator without reading it (mainloop-only timing)
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
-            continue;
-#endif
             if (my_last < 0) {   // no chunk for this warp in a narrow tile: release TMEM right away
                 tc_fence_before();
                 __syncwarp();
@@ -433,10 +423,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
                 }
-#ifdef DMPQ_EPI_LDONLY   // development: read the accumulator, skip the math and the stores
-                if (r[0] == 0x7FFFFFFFu && p.Y32) p.Y32[0] = 0.0f;
-                continue;
-#endif
                 const int col0 = n0 + c * 32;
                 f2 y[16];
 #pragma unroll
@@ -543,21 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                                                      ((col0 >> 4) & 3)) = (uint16_t)sc;
                     }
                 }
-#ifdef DMPQ_EPI_NOSTORE   // development: the epilogue math without the bf16 output stores
-                if (yb[0] == 0x7FFFFFFFu && yb[15] == 0x7FFFFFFFu && p.Y32) p.Y32[0] = 0.0f;
-                if (false) {
-#elif defined(DMPQ_EPI_DIRECT)   // development: bf16 output stored from registers (lane = row, 64 B per lane)
-                if (p.Y && !tma_res) {
-                    if (row_ok) {
-                        uint4* yp = reinterpret_cast<uint4*>(p.Y + (size_t)row * p.ldy + col0);
-#pragma unroll
-                        for (int v4 = 0; v4 < 4; ++v4)
-                            yp[v4] = make_uint4(yb[4 * v4], yb[4 * v4 + 1], yb[4 * v4 + 2], yb[4 * v4 + 3]);
-                    }
-                } else if (p.Y) {
-#else
                 if (p.Y) {
-#endif
                     if (!tma_res) {
                         if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
                             if constexpr (L::STAGING_BUFS == 3) bulk_wait_read2();
@@ -573,38 +545,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                                      "r"(yb[4 * v4 + 1]), "r"(yb[4 * v4 + 2]), "r"(yb[4 * v4 + 3])
                                      : "memory");
                     }
-#ifdef DMPQ_EPI_LSU
-                    // coalesced LSU stores of the staged chunk (no TMA store): 16-byte pieces, eight
-                    // rows of 64 B per warp instruction
-                    __syncwarp();
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int pc = i * 32 + lane, rr = pc >> 2, part = pc & 3;
-                        uint4 v;
-                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                     : "r"(buf + rr * 64 + ((uint32_t)(part ^ ((rr >> 1) & 3)) << 4)) : "memory");
-                        if (rowbase + rr < p.m)
-                            *reinterpret_cast<uint4*>(p.Y + (size_t)(rowbase + rr) * p.ldy + col0 + part * 8) = v;
-                    }
-                    __syncwarp();
-                    if (lane == 0 && tma_res && jc + NSB < nmine) {   // the buffer's next residual chunk
-                        fence_proxy_async_smem();
-                        res_load(jc + NSB);
-                    }
-#else
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                            if (DMPQ_GEMM_L2HINT) tma_store_2d_hint(&tmY, buf, col0, rowbase, l2_policy_evict_first());
-                        else tma_store_2d(&tmY, buf, col0, rowbase);
+                            tma_store_2d(&tmY, buf, col0, rowbase);
                         bulk_commit();
                         if (tma_res && jc + NSB < nmine) {   // this buffer's next residual chunk, once the store has read it
                             bulk_wait_read0();
                             res_load(jc + NSB);
                         }
                     }
-#endif
                     ++chunk_ctr;
                 }
                 if (has_tdc && row_ok) {
