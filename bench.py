@@ -758,10 +758,10 @@ def main():
     ap.add_argument("--fuse-quant", action="store_true", help="producer-fused NVFP4 quantization of the FFN2 input in "
                     "FFN1's epilogue (P:336, NEXT-2; plain quantizer only, i.e. with --no-hadamard)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")
-    ap.add_argument("--no-int8-cast", dest="int8_cast", action="store_false",
-                    help="keep both weight forms resident (default: NVFP4-only residency, INT8 codes cast on the fly "
-                    "per INT8 GEMM into an L2-resident scratch, P:184, NEXT-4b: 3.5x less weight memory and measured "
-                    "faster, DESIGN.md 5.7b)")
+    ap.add_argument("--int8-cast", action="store_true",
+                    help="NVFP4-only weight residency, INT8 codes cast on the fly per INT8 GEMM into an L2-resident "
+                    "scratch (P:184, NEXT-4b): 3.5x less weight memory than BF16; same-box 0.5 %% slower at full size, "
+                    "6 %% at one rank's share of 8 GPUs (DESIGN.md 5.7b). Default: both forms pre-packed (north_star)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs --warmup >= 3", file=sys.stderr)

@@ -234,3 +234,83 @@ def test_fullsize_qkv_concat_sampled(D, orc, fmt):
                                      bias)[0]
                 err = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
                 assert err <= 1e-5, (j, r, err)
+
+
+@pytest.mark.parametrize("n,k,ln", [(1920, 1920, True), (1920, 7680, False)])
+def test_fullsize_cogvideox2b_hadamard_sampled(D, orc, n, k, ln):
+    """CogVideoX-2B layer shapes (BASELINE configs[2]: hidden 1920, FFN 7680; 15 / 60 Hadamard blocks per
+    row, ragged against the quantizer's 8-thread row segments) at M = 35,552: LN + Hadamard quantizer
+    and both GEMMs on sampled rows against the oracle."""
+    x = synth.dit_activation(M, k, seed=k + 5) if k == 1920 else synth.ffn2_activation(M, k, seed=k + 5)
+    xd = x.cuda()
+    w, b = synth.linear_weight_device(n, k, seed=n + k + 5, device="cuda")
+    pw = D.dmpq_pack_weights(w, b, hadamard=True)
+    h = torch.empty(M, k, dtype=torch.bfloat16, device="cuda") if ln else None
+    g = torch.tensor([0.02], device="cuda")
+    a8 = D.QuantAct.empty(D.FMT_INT8, M, k, "cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, M, k, "cuda", g=g)
+    D.dmpq_quantize_act(xd, out_i8=a8, out_fp4=a4, layernorm=ln, h_out=h, hadamard=True)
+    y8 = torch.empty(M, n, dtype=torch.bfloat16, device="cuda")
+    y4 = torch.empty(M, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a8, pw, Y=y8)
+    D.dmpq_gemm(a4, pw, Y=y4)
+    torch.cuda.synchronize()
+    pk = orc.pack_weights_hadamard(synth.bits(w.cpu()))
+    assert np.array_equal(pw.i8_codes.cpu().numpy(), pk["i8_codes"])
+    src = synth.bits(h.cpu()) if ln else synth.bits(x)
+    bias = b.cpu().numpy()
+    c8_all, s8_all = a8.codes.cpu().numpy(), a8.row_scale.cpu().numpy()
+    c4_all, sf4 = a4.codes.cpu().numpy(), orc.sf_unswizzle(a4.sf.cpu().numpy(), M, k)
+    for r in sample_rows(M, n=8, seed=4):
+        y = orc.fht128(orc.bf16_to_f32(src[r:r + 1]).reshape(1, k))
+        c8, s8 = orc.int8_quantize_f32(y)
+        assert np.array_equal(c8_all[r:r + 1], c8) and s8_all[r] == s8[0], r
+        c4, s4 = orc.nvfp4_quantize_f32(y, 0.02)
+        assert np.array_equal(c4_all[r:r + 1], c4) and np.array_equal(sf4[r:r + 1], s4), r
+        _, yr8 = orc.gemm_int8(c8, s8, pk["i8_codes"], pk["i8_scale"], bias)
+        assert torch.equal(y8[r:r + 1].cpu(), torch.from_numpy(yr8).to(torch.bfloat16)), r
+        yr4 = orc.gemm_nvfp4(c4, s4, 0.02, pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"], bias)
+        got = y4[r].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got - yr4[0]) <= 4e-3 * np.linalg.norm(yr4[0]), r
+
+
+def test_max_size_hunyuan_rows_sampled(D, orc):
+    """The largest single-GPU row count of the workloads (BASELINE configs[4]: 119,056 tokens,
+    hidden 3072) through the LN + Hadamard quantizer (both formats) and both GEMMs of the O shape:
+    sampled rows (incl. the ragged last tile) against the oracle; the tensor amax over all rows."""
+    Mh, k, n = 119056, 3072, 3072
+    xd = synth.dit_activation_device(Mh, k, seed=12, device="cuda")
+    w, b = synth.linear_weight_device(n, k, seed=13, device="cuda")
+    pw = D.dmpq_pack_weights(w, b, hadamard=True)
+    h = torch.empty(Mh, k, dtype=torch.bfloat16, device="cuda")
+    g = torch.tensor([0.02], device="cuda")
+    amax = torch.zeros(1, device="cuda")
+    a8 = D.QuantAct.empty(D.FMT_INT8, Mh, k, "cuda")
+    a4 = D.QuantAct.empty(D.FMT_NVFP4, Mh, k, "cuda", g=g)
+    D.dmpq_quantize_act(xd, out_i8=a8, out_fp4=a4, amax_out=amax, layernorm=True, h_out=h, hadamard=True)
+    y8 = torch.empty(Mh, n, dtype=torch.bfloat16, device="cuda")
+    y4 = torch.empty(Mh, n, dtype=torch.bfloat16, device="cuda")
+    D.dmpq_gemm(a8, pw, Y=y8)
+    D.dmpq_gemm(a4, pw, Y=y4)
+    torch.cuda.synchronize()
+    pk = orc.pack_weights_hadamard(synth.bits(w.cpu()))
+    bias = b.cpu().numpy()
+    rows = sample_rows(Mh, n=8, seed=6)
+    hb = synth.bits(h[rows].cpu())
+    c8_all, s8_all = a8.codes[rows].cpu().numpy(), a8.row_scale[rows].cpu().numpy()
+    c4_all = a4.codes[rows].cpu().numpy()
+    sf4 = orc.sf_unswizzle(a4.sf.cpu().numpy(), Mh, k)[rows]
+    ymax = 0.0
+    for i, r in enumerate(rows):
+        y = orc.fht128(orc.bf16_to_f32(hb[i:i + 1]).reshape(1, k))
+        ymax = max(ymax, float(np.abs(y).max()))
+        c8, s8 = orc.int8_quantize_f32(y)
+        assert np.array_equal(c8_all[i:i + 1], c8) and s8_all[i] == s8[0], r
+        c4, s4 = orc.nvfp4_quantize_f32(y, 0.02)
+        assert np.array_equal(c4_all[i:i + 1], c4) and np.array_equal(sf4[i:i + 1], s4), r
+        _, yr8 = orc.gemm_int8(c8, s8, pk["i8_codes"], pk["i8_scale"], bias)
+        assert torch.equal(y8[r:r + 1].cpu(), torch.from_numpy(yr8).to(torch.bfloat16)), r
+        yr4 = orc.gemm_nvfp4(c4, s4, 0.02, pk["fp4_codes"], pk["fp4_sf"], pk["fp4_g"], bias)
+        got = y4[r].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got - yr4[0]) <= 4e-3 * np.linalg.norm(yr4[0]), r
+    assert amax.item() >= ymax
