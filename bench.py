@@ -560,6 +560,14 @@ def run_ours(args):
                  "exchange": brk["exchange"] / args.steps * 1e3, "int8_cast": brk["cast"] / args.steps * 1e3}
     breakdown["host_gaps_and_other"] = elapsed_b / args.steps * 1e3 - sum(breakdown.values())
     breakdown["pass"] = "eager replay of the timed steps with per-launch CUDA events"
+    # in-step HBM-bound kernels: algorithmic bytes / their CUDA-event time, against the measured copy peak
+    hbm_kernels = {}
+    for kind in ("quantize", "tdc", "cast"):
+        secs = brk[kind]
+        if secs > 0:
+            gbs = model.hbm_bytes[kind] / secs / 1e9
+            hbm_kernels[kind] = {"bytes_per_step": model.hbm_bytes[kind] / args.steps, "ms_per_step": secs / args.steps * 1e3,
+                                 "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"]}
 
     # ---- pass C (e2e): the same steps through host buffers (pinned H2D of each step's input,
     # D2H of its output), graphs as in pass A. The copies run on a second stream, double-
@@ -693,6 +701,7 @@ def run_ours(args):
         "paper_context": PAPER_CONTEXT,
         "bounds": bounds,
         "breakdown_ms_per_step": breakdown,
+        "hbm_kernels_in_step": hbm_kernels,
         "effective_tflops_dense_equiv": dense_flops / elapsed / 1e12,
         "wall_s_timed": wall,
         "host_issue_ms_per_step": host_issue / args.steps * 1e3,

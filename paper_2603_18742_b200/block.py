@@ -208,6 +208,7 @@ class DiTStack:
         self.launches = 0                       # libdmpq kernel launches issued (bench's gpu_launches)
         self.timing = False                     # record CUDA events around every GEMM (roofline)
         self.kernel_events = {"quantize": [], "tdc": [], "exchange": [], "cast": []}   # breakdown of the step
+        self.hbm_bytes = {"quantize": 0.0, "tdc": 0.0, "cast": 0.0}   # algorithmic HBM bytes of those kernels (timing passes)
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
         self.capture = None                     # dict -> per-stage clones for the parity tests
@@ -269,6 +270,14 @@ class DiTStack:
                             h_out=h_buf if want_h else None, hadamard=self.hadamard,
                             row_abs_sum=self.row_abs[b * N_SLOTS + slot] if self.pdr else None,
                             amax_in=self.amax[1, b, slot:slot + 1] if self.pdr else None)
+        if self.timing:   # algorithmic HBM bytes of this launch (the bench's in-step quantizer GB/s)
+            m, k = src.shape
+            nb = 2 * m * k + (2 * m * k if want_h else 0)
+            if a4 is not None:
+                nb += m * k // 2 + m * k // 16
+            if a8 is not None:
+                nb += m * k + 4 * (m * k // 128 if a8.scale_block else m)
+            self.hbm_bytes["quantize"] += nb
         out = {D.FMT_INT8: a8, D.FMT_NVFP4: a4}
         if D.FMT_BF16 in fmts_needed:
             out[D.FMT_BF16] = D.QuantAct.bf16(h_buf if layernorm else src)
@@ -376,6 +385,8 @@ class DiTStack:
         if a.fmt == D.FMT_INT8 and self.int8_cast:   # rebuild this layer's INT8 codes from its NVFP4 form
             with self._ev("cast"):
                 w = D.dmpq_cast_int8(w, self.i8_scratch)
+            if self.timing:   # NVFP4 codes + scales read, INT8 codes written
+                self.hbm_bytes["cast"] += 1.5625 * w.n * w.k
         if self.timing:
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
@@ -394,6 +405,7 @@ class DiTStack:
         return out
 
     def reset_timing(self):
+        self.hbm_bytes = {"quantize": 0.0, "tdc": 0.0, "cast": 0.0}
         self.kernel_events = {"quantize": [], "tdc": [], "exchange": [], "cast": []}
         self.gemm_events = {D.FMT_INT8: [], D.FMT_NVFP4: [], D.FMT_BF16: []}
         self.gemm_flops = {D.FMT_INT8: 0.0, D.FMT_NVFP4: 0.0, D.FMT_BF16: 0.0}
@@ -416,8 +428,14 @@ class DiTStack:
         self.g_delta.zero_()
         self.records = []
 
+    def _tdc_bytes(self, refresh: bool):
+        if self.timing:   # refresh: X_in, X_out, Delta_prev read + Delta_new written; skip: X_in, Delta read + X_out
+            self.hbm_bytes["tdc"] += (8 if refresh else 6) * self.m * self.H if not self.cache_nvfp4 else \
+                (4 + 2 * 0.5625 if refresh else 4.5625) * self.m * self.H
+
     def _refresh(self, b, x_in, x_out):
         """tdc_step(REFRESH) of block b (bf16 cache): Delta_b, the block's FP64 statistics."""
+        self._tdc_bytes(True)
         with self._ev("tdc"):
             D.tdc_step(L.TDC_REFRESH, x_in, x_out, self.delta[b], self.stats_slots[self.rank, b, :L.STATS_LEN],
                        self.ws.tdc_ws)
@@ -426,6 +444,7 @@ class DiTStack:
         """Enqueue one block's kernels (capturable: no host sync, no allocation). refresh=False leaves
         a computed block's TDC refresh to the caller (overlapped on the side stream)."""
         if d == L.TDC_DECIDE_SKIP:
+            self._tdc_bytes(False)
             with self._ev("tdc"):
                 if self.cache_nvfp4:
                     D.tdc_step_nvfp4(L.TDC_SKIP, x_in, x_out, self.delta[b])
@@ -438,6 +457,7 @@ class DiTStack:
         flops = self._compute_block(b, x_in, x_out, fmts)
         if not refresh:
             return flops
+        self._tdc_bytes(True)
         with self._ev("tdc"):
             if self.cache_nvfp4:
                 am, g = self.delta_amax[b:b + 1], self.g_delta[b:b + 1]
