@@ -566,8 +566,11 @@ def test_quantize_hadamard_layernorm_no_h(D, orc, k, which):
         assert np.array_equal(a4.codes.cpu().numpy(), c4)
 
 
-@pytest.mark.parametrize("had,overlap", [(True, False), (False, False), (True, True)])
-def test_graph_replay_equals_eager(D, had, overlap):
+@pytest.mark.parametrize("had,overlap,extra", [(True, False, {}), (False, False, {}), (True, True, {}),
+                                               (True, False, {"pdr": "current", "tau_outlier": 9.0}),
+                                               (True, False, {"int8_cast": True, "int8_block": True}),
+                                               (False, False, {"fuse_quant": True, "tau_gamma": [0.05] * 6})])
+def test_graph_replay_equals_eager(D, had, overlap, extra):
     """The bench's headline pass replays one CUDA graph per (block, decision, formats) pattern.
     Six timesteps of a two-block stack replayed from graphs equal the same steps launched eagerly
     bit for bit: outputs of every step, delta caches, FP64 statistics, global scales, decisions;
@@ -579,7 +582,7 @@ def test_graph_replay_equals_eager(D, had, overlap):
     runs = []
     for graphs in (False, True):
         stack = DiTStack(3 if overlap else 2, H, F, M, "cuda", seed=4, gate_scales=[0.008, 0.012, 0.006][:3 if overlap else 2],
-                         hadamard=had, tdc_cfg=(0.001, 0.02, 2), overlap_refresh=overlap)
+                         hadamard=had, tdc_cfg=(0.001, 0.02, 2), overlap_refresh=overlap, **extra)
         stack.use_graphs = graphs
         outs, stats = [], []
         for t in range(T):
@@ -593,7 +596,8 @@ def test_graph_replay_equals_eager(D, had, overlap):
     assert g["graphs"] > 0 and e["graphs"] == 0
     assert e["dec"] == g["dec"] and e["fmts"] == g["fmts"]
     assert any(d == 1 for ds in e["dec"] for d in ds), "the trajectory should skip at least once"
-    assert {f for fs in e["fmts"] for ff in fs if ff for f in ff} >= {0, 1}, "both formats should run"
+    assert {f for fs in e["fmts"] for ff in fs if ff for f in ff} >= ({0, 2} if extra.get("pdr") else {0, 1}), \
+        "both formats should run"
     for a, b in zip(e["outs"], g["outs"]):
         assert torch.equal(a, b)
     for a, b in zip(e["stats"], g["stats"]):
