@@ -438,6 +438,7 @@ def run_ours(args):
     from paper_2603_18742_b200 import synth
     from paper_2603_18742_b200.block import DiTStack
     from paper_2603_18742_b200.shard import shard_rows
+    from paper_2603_18742_b200._lib import TDC_METRIC_COS as L_TDC_COS, TDC_METRIC_REL_L2 as L_TDC_REL_L2
 
     build.build()
     rank, world, local, group = dist_setup(args)
@@ -456,10 +457,12 @@ def run_ours(args):
     T = max(T, args.warmup + args.steps)
     peaks, peak_kind = load_peaks()
 
-    model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard,
+    tdc_cfg = (0.001, args.tdc_tau if args.tdc_tau is not None else 0.003, 2,
+               {"cos": L_TDC_COS, "rel_l2": L_TDC_REL_L2}[args.tdc_metric])
+    model = DiTStack(nb, H, F, m, dev, seed=args.seed, group=group, hadamard=not args.no_hadamard, tdc_cfg=tdc_cfg,
                      pdr={None: False, "delayed": True, "current": "current"}[args.pdr], m_total=M, cache_nvfp4=args.cache_nvfp4, fuse_refresh=args.fused_refresh,
                      int8_cast=args.int8_cast, int8_block=args.int8_block, fuse_quant=args.fuse_quant,
-                     overlap_refresh=args.overlap_refresh)
+                     overlap_refresh=args.overlap_refresh, g_policy=args.g_policy)
     # block-0 input trajectory basis: ONE seeded global [M x H] input, of which this rank takes its
     # contiguous row shard -- every world size solves the same problem (same mix, same decisions)
     A, B = synth.trajectory_basis(M, H, seed=1000 + args.seed, device=dev)
@@ -689,7 +692,8 @@ def run_ours(args):
                    "device_map": os.environ.get("DMPQ_DEVICE_MAP", "one GPU per rank"),
                    "input": "one seeded global input; each rank takes its contiguous row shard", "l2": "inputs larger than L2 (multi-GB working set per step)",
                    "cuda_graphs": not args.no_graphs, "tdc_refresh": "fused in the FFN2 GEMM epilogue" if model.fuse_refresh else "own kernel",
-                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr or False, "int8_weight_cast": args.int8_cast, "producer_fused_quant": model.fuse_quant,
+                   "hadamard": not args.no_hadamard, "pdr_outlier_gate": args.pdr or False, "int8_weight_cast": args.int8_cast, "producer_fused_quant": model.fuse_quant, "nvfp4_g_policy": args.g_policy,
+                   "tdc": {"rho": tdc_cfg[0], "tau": tdc_cfg[1], "n_max": tdc_cfg[2], "metric": args.tdc_metric},
                    "tdc_refresh_overlap": model.overlap_refresh,
                    "int8_granularity": "per 128-block (R17)" if args.int8_block else "per token (R2)",
                    "delta_cache": {"format": "nvfp4" if args.cache_nvfp4 else "bf16",
@@ -764,6 +768,12 @@ def main():
                     "Hadamard blocks (P:187, R17, NEXT-1) instead of per-token INT8")
     ap.add_argument("--overlap-refresh", action="store_true", help="run each block's TDC refresh on a side stream "
                     "overlapped with the next block (measured no faster; DESIGN.md 5.4)")
+    ap.add_argument("--g-policy", default="delayed", choices=["delayed", "current"], help="NVFP4 per-tensor scale "
+                    "(R3): delayed (previous step's amax / 1344, the default) or current (an amax pass over each "
+                    "NVFP4-quantized input first, amax / 2688; single rank)")
+    ap.add_argument("--tdc-metric", default="cos", choices=["cos", "rel_l2"], help="the distance D of Eq. 9 (P:215): "
+                    "1 - CosSim (the paper's default) or the relative-L2 distance (R19)")
+    ap.add_argument("--tdc-tau", type=float, default=None, help="TDC threshold tau (P:255: 0.003)")
     ap.add_argument("--fuse-quant", action="store_true", help="producer-fused NVFP4 quantization of the FFN2 input in "
                     "FFN1's epilogue (P:336, NEXT-2; plain quantizer only, i.e. with --no-hadamard)")
     ap.add_argument("--cache-nvfp4", action="store_true", help="NVFP4-compressed TDC delta cache (P:226, R16, NEXT-4)")

@@ -226,7 +226,9 @@ typedef struct {
  *  INT8 per token (R2): a = max_k|x|; s = fl(a/127); code =
  *    RNE(fl(x*fl(127/a))); a == 0 gives s = 1 and zero codes.
  *  Either output may be NULL; both may be NULL when opts asks for h_out or the PDR
- *  statistics only (a BF16-routed tensor, R15). out->m/k must equal m/k.
+ *  statistics only (a BF16-routed tensor, R15), or for an amax-only pass (the "current"
+ *  global-scale policy, R3: amax first, then g = max(fl(amax/2688), FLT_MIN), then quantize).
+ *  out->m/k must equal m/k.
  *  amax_out: if non-NULL, device FP32 that receives max(*amax_out, max|x|)
  *  (atomic; the caller zeroes it once per step). With DMPQ_QF_LAYERNORM the
  *  quantised (and amax'd) values are the bf16-rounded normalised rows.
@@ -383,10 +385,15 @@ typedef struct {
     int n_computed;   /* computed deltas so far (warm-up needs two)    */
 } tdc_state;
 
+typedef enum { TDC_METRIC_COS = 0, TDC_METRIC_REL_L2 = 1 } tdc_metric;
+
 typedef struct {
     double rho;       /* 0.001 */
     double tau;       /* 0.003 */
     int n_max;        /* 2     */
+    int metric;       /* the distance D of Eq. 9: TDC_METRIC_COS = 1 - CosSim (the paper's
+                         default, 0 when zero-initialised) or TDC_METRIC_REL_L2 ("relative-L2
+                         distance", R19): ||Delta_t - Delta_prev||_2 / ||Delta_prev||_2 */
 } tdc_config;
 
 void tdc_init(tdc_state* st);
@@ -398,7 +405,9 @@ tdc_decision tdc_decide(const tdc_state* st, const tdc_config* cfg, int t);
 /* Eq. 10 at the end of step t. After a Compute, `st_global` holds the
  * block's global statistics from tdc_step(REFRESH) and
  * E_{t_p} = 1 - dot_dd / sqrt(sum_dn2 * sum_dp2) (Eq. 9; +INF when a norm
- * is zero or this is the first compute); e_acc = E_{t_p}; t_p = t. After a
+ * is zero or this is the first compute), or with TDC_METRIC_REL_L2
+ * E_{t_p} = sqrt(max(sum_dn2 - 2 dot_dd + sum_dp2, 0)) / sqrt(sum_dp2) (+INF when
+ * sum_dp2 is zero or this is the first compute); e_acc = E_{t_p}; t_p = t. After a
  * Skip, e_acc = (e_acc + e_tp) + rho (st_global ignored, may be NULL). */
 void tdc_update(tdc_state* st, const tdc_config* cfg, int t, tdc_decision d, const dmpq_block_stats* st_global);
 

@@ -34,6 +34,8 @@ from .decisions import (  # noqa: F401  (re-export)
     tdc_decide,
     tdc_update,
     cosine_error_from_stats,
+    prediction_error_from_stats,
+    rel_l2_error_from_stats,
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

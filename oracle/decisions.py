@@ -79,12 +79,30 @@ def cosine_error_from_stats(dot: float, n_new: float, n_prev: float) -> float:
     return 1.0 - dot / math.sqrt(n_new * n_prev)
 
 
+def rel_l2_error_from_stats(dot: float, n_new: float, n_prev: float) -> float:
+    """Eq. 9 with D = relative-L2 distance (P:215 "other metrics such as relative-L2 distance";
+    reading R19): ||Delta_t - Delta_prev||_2 / ||Delta_prev||_2, with ||a - b||^2 expanded as
+    ||a||^2 - 2 a.b + ||b||^2 (the three sums the refresh produces). A zero reference norm is
+    maximal error (+inf), as for the cosine."""
+    if n_prev == 0.0:
+        return math.inf
+    return math.sqrt(max(n_new - 2.0 * dot + n_prev, 0.0)) / math.sqrt(n_prev)
+
+
+def prediction_error_from_stats(st, metric: str = "cos") -> float:
+    """E_{t_p} of Eq. 9 from a block's statistics (dot, ||Delta_t||^2, ||Delta_prev||^2 at [4:7])."""
+    if metric == "rel_l2":
+        return rel_l2_error_from_stats(st[4], st[5], st[6])
+    return cosine_error_from_stats(st[4], st[5], st[6])
+
+
 @dataclass
 class TdcConfig:
-    """P:255: rho = 0.001, N_max = 2, tau = 0.003."""
+    """rho = 0.001, N_max = 2, tau = 0.003; D of Eq. 9: "cos" (default) or "rel_l2"."""
     rho: float = 0.001
     tau: float = 0.003
     n_max: int = 2
+    metric: str = "cos"
 
 
 @dataclass

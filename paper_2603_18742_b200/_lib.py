@@ -25,6 +25,7 @@ EP_BIAS, EP_GELU_TANH, EP_RESIDUAL, EP_TDC_REFRESH, EP_QUANT_NVFP4 = 1, 2, 4, 8,
 TDC_SKIP, TDC_REFRESH = 0, 1
 TDC_COMPUTE, TDC_DECIDE_SKIP = 0, 1
 GAMMA_L1, GAMMA_L2 = 0, 1
+TDC_METRIC_COS, TDC_METRIC_REL_L2 = 0, 1
 STATS_LEN = 7
 
 
@@ -71,7 +72,7 @@ class TdcState(ctypes.Structure):
 
 
 class TdcConfig(ctypes.Structure):
-    _fields_ = [("rho", c_double), ("tau", c_double), ("n_max", c_int)]
+    _fields_ = [("rho", c_double), ("tau", c_double), ("n_max", c_int), ("metric", c_int)]
 
 
 # every function the header declares (checked against include/dmpq.h by the tests)

@@ -24,6 +24,7 @@ statistics and maxima are combined across ranks with ONE slot-packed SUM all-red
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -35,6 +36,7 @@ from . import synth
 from .shard import SlotBuffer, combine_host, exchange_device
 
 LAYERS = ("q", "k", "v", "o", "ffn1", "ffn2")
+NVTX = os.environ.get("DMPQ_NVTX") == "1"   # NVTX ranges per step and block (for nsys / ncu range filters)
 N_STATS = L.STATS_LEN + 4      # per block: 7 TDC/predictor sums + sum|x| of the 4 layer inputs (PDR, R15)
 SLOT_OF_LAYER = (0, 0, 0, 1, 2, 3)   # activation tensor each layer consumes
 N_SLOTS = 4
@@ -130,7 +132,7 @@ class DiTStack:
                  force_fmt: int | None = None, group=None, hadamard: bool = False, pdr: bool = False,
                  tau_outlier: float = 25.0, m_total: int | None = None, cache_nvfp4: bool = False,
                  fuse_refresh: bool = False, fuse_qkv: bool = True, int8_cast: bool = False, int8_block: bool = False,
-                 fuse_quant: bool = False, overlap_refresh: bool = False):
+                 fuse_quant: bool = False, overlap_refresh: bool = False, g_policy: str = "delayed"):
         self.nb, self.H, self.F, self.m = n_blocks, H, F, m_local
         self.device = torch.device(device)
         self.cfg = L.TdcConfig(*tdc_cfg)
@@ -159,16 +161,27 @@ class DiTStack:
         if int8_block and not hadamard:
             raise ValueError("per-block INT8 (R17) is defined on the Hadamard blocks: needs hadamard=True")
         self.int8_block = int8_block
+        # NVFP4 per-tensor scale (R3): "delayed" = max(fl(amax_{t-1}/1344), FLT_MIN) from the previous
+        # step's (all-rank) amax, the default; "current" = an amax-only pass over this input first,
+        # then max(fl(amax/2688), FLT_MIN) -- one extra read of each NVFP4-quantized tensor, and a
+        # per-tensor cross-rank maximum inside the block under sharding, so single-rank only
+        if g_policy not in ("delayed", "current"):
+            raise ValueError("g_policy must be 'delayed' or 'current'")
+        if g_policy == "current" and group is not None and torch.distributed.get_world_size(group) > 1:
+            raise ValueError("g_policy='current' is single-rank (it needs a cross-rank max per NVFP4 tensor)")
+        self.g_policy = g_policy
         # producer-fused quantization (NEXT-2): FFN1's epilogue writes the NVFP4 codes of the
         # FFN2 input directly (no bf16 f round trip, no standalone quantizer) when FFN2 is routed
         # NVFP4; built for the plain quantizer (the Hadamard blocks do not fit the epilogue, DESIGN 5.7)
-        self.fuse_quant = fuse_quant and not hadamard and not pdr
+        # (not with the "current" g policy: FFN2's global scale would need f's amax before f exists)
+        self.fuse_quant = fuse_quant and not hadamard and not pdr and g_policy == "delayed"
         if gate_scales is None:
             gate_scales = [0.004 * (1 + (b % 5)) for b in range(n_blocks)]
         self.blocks = [make_block_weights(H, F, seed * 1000 + b, self.device, gate_scales[b], hadamard, keep_bf16=pdr,
                                           fuse_qkv=fuse_qkv, int8_resident=not int8_cast) for b in range(n_blocks)]
         self.i8_scratch = torch.empty(max(3 * H * H, F * H) if int8_cast else 0, dtype=torch.int8, device=self.device)
         self.g_table = torch.ones(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
+        self.g_cur_amax = torch.zeros(n_blocks, N_SLOTS, dtype=torch.float32, device=self.device)
         # one buffer for the per-step MAX all-reduce: [0] amax of the quantised values (NVFP4 global
         # scales, R3); [1] max|x| of the layer inputs (PDR, R15); then max|d| of each block's last
         # refresh (compressed delta cache, R16; kept across steps: skipped blocks do not refresh)
@@ -266,6 +279,13 @@ class DiTStack:
         want_h = layernorm and (D.FMT_BF16 in fmts_needed or self.capture is not None or self.pdr_current)
         a8 = ws.act(slot, D.FMT_INT8, b) if D.FMT_INT8 in fmts_needed else None
         a4 = ws.act(slot, D.FMT_NVFP4, b) if D.FMT_NVFP4 in fmts_needed else None
+        if a4 is not None and self.g_policy == "current":   # R3 "current": amax pass, then g from it
+            am = self.g_cur_amax[b, slot:slot + 1]
+            am.zero_()
+            D.dmpq_quantize_act(src, amax_out=am, layernorm=layernorm, hadamard=self.hadamard)
+            D.dmpq_global_scale(am, 2688.0, self.g_table[b, slot:slot + 1])
+            if self.timing:
+                self.hbm_bytes["quantize"] += 2 * src.numel()
         D.dmpq_quantize_act(src, out_i8=a8, out_fp4=a4, amax_out=self.amax[0, b, slot:slot + 1], layernorm=layernorm,
                             h_out=h_buf if want_h else None, hadamard=self.hadamard,
                             row_abs_sum=self.row_abs[b * N_SLOTS + slot] if self.pdr else None,
@@ -487,7 +507,13 @@ class DiTStack:
         if overlap:   # this step's refreshes start after the statistics slots were zeroed
             self.refresh_stream.wait_stream(main)
         pending = set()   # blocks whose refresh of this step was enqueued on the side stream
+        if NVTX:
+            torch.cuda.nvtx.range_push(f"dmpq step t={t}")
         for b in range(self.nb):
+            if NVTX:
+                if b:
+                    torch.cuda.nvtx.range_pop()
+                torch.cuda.nvtx.range_push(f"block {b}")
             x_out = self.x_buf[b % len(self.x_buf)]
             if overlap and (b - 2) in pending:   # block b overwrites the buffers refresh(b - 2) reads
                 main.wait_event(self.ev_refreshed[b - 2])
@@ -551,6 +577,10 @@ class DiTStack:
                     self.launches -= 1
                 if self.pdr_current:   # + 4 device gates + the predicated-off GEMM of every layer
                     self.launches += 4 + 6
+                if self.g_policy == "current":   # amax pass + global scale per NVFP4-quantized input
+                    nv = [any(f == D.FMT_NVFP4 for f in fmts[0:3]), fmts[3] == D.FMT_NVFP4, fmts[4] == D.FMT_NVFP4,
+                          fmts[5] == D.FMT_NVFP4]
+                    self.launches += 2 * sum(nv)
                 if self.int8_cast:   # one cast per INT8 GEMM launch
                     i8 = [f == D.FMT_INT8 for f in fmts]
                     self.launches += (int(i8[0]) if qkv1 else sum(i8[0:3])) + sum(i8[3:6])
@@ -561,6 +591,10 @@ class DiTStack:
             x_in = x_out
         if overlap:   # join: the exchange and the next step see every refresh
             main.wait_stream(self.refresh_stream)
+        if NVTX:
+            if self.nb:
+                torch.cuda.nvtx.range_pop()
+            torch.cuda.nvtx.range_pop()
         self.records.append(rec)
         return x_in
 
@@ -576,9 +610,10 @@ class DiTStack:
             # one SUM all-reduce of the slot buffer (statistics + maxima): every rank then holds
             # every rank's partial sums and the global maxima
             exchange_device(self.slots, self.amax_all, self.group)
-            # next step's NVFP4 global scales from the (all-rank) amax of this step (R3)
-            D.dmpq_global_scale(self.amax[0].view(-1), 1344.0, self.g_table.view(-1))
-            self.launches += 1
+            # next step's NVFP4 global scales from the (all-rank) amax of this step (R3, delayed policy)
+            if self.g_policy == "delayed":
+                D.dmpq_global_scale(self.amax[0].view(-1), 1344.0, self.g_table.view(-1))
+                self.launches += 1
             if self.cache_nvfp4:   # delta-cache scales for each block's next refresh (same delayed policy)
                 D.dmpq_global_scale(self.delta_amax, 1344.0, self.g_delta)
                 self.launches += 1

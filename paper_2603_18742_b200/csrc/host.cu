@@ -139,8 +139,12 @@ extern "C" tdc_decision tdc_decide(const tdc_state* st, const tdc_config* cfg, i
 extern "C" void tdc_update(tdc_state* st, const tdc_config* cfg, int t, tdc_decision d, const dmpq_block_stats* g) {
     if (d == TDC_COMPUTE) {
         double e = INFINITY;
-        if (st->n_computed > 0 && g != nullptr && g->sum_dn2 != 0.0 && g->sum_dp2 != 0.0)
+        if (cfg->metric == TDC_METRIC_REL_L2) {   // ||Delta_t - Delta_prev|| / ||Delta_prev|| (R19)
+            if (st->n_computed > 0 && g != nullptr && g->sum_dp2 != 0.0)
+                e = std::sqrt(std::fmax(g->sum_dn2 - 2.0 * g->dot_dd + g->sum_dp2, 0.0)) / std::sqrt(g->sum_dp2);
+        } else if (st->n_computed > 0 && g != nullptr && g->sum_dn2 != 0.0 && g->sum_dp2 != 0.0) {
             e = 1.0 - g->dot_dd / std::sqrt(g->sum_dn2 * g->sum_dp2);
+        }
         st->e_tp = e;
         st->e_acc = e;
         st->t_p = t;

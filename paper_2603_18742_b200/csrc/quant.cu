@@ -60,9 +60,9 @@ using namespace dmpq;
 
 extern "C" dmpq_status dmpq_quantize_act(const uint16_t* X, int m, int k, int ldx, const dmpq_quant_opts* opts,
                                          dmpq_act* out_i8, dmpq_act* out_fp4, float* amax_out, dmpq_stream_t s) {
-    DMPQ_REQUIRE(out_i8 || out_fp4 ||
+    DMPQ_REQUIRE(out_i8 || out_fp4 || amax_out ||
                      (opts && ((opts->flags & DMPQ_QF_WRITE_H) || opts->row_abs_sum || opts->amax_in)),
-                 DMPQ_EINVAL, "dmpq_quantize_act: nothing to produce (no output, h_out or statistics)");
+                 DMPQ_EINVAL, "dmpq_quantize_act: nothing to produce (no output, amax, h_out or statistics)");
     DMPQ_REQUIRE(m >= 0 && k > 0 && k % 64 == 0 && k <= 16384, DMPQ_ESHAPE,
                  "dmpq_quantize_act: need k %% 64 == 0, 0 < k <= 16384, m >= 0 (m=%d k=%d)", m, k);
     DMPQ_REQUIRE(ldx >= k && ldx % 8 == 0, DMPQ_EALIGN, "dmpq_quantize_act: ldx=%d must be >= k and a multiple of 8", ldx);

@@ -96,13 +96,14 @@ def test_predict_matches_oracle(L, orc):
     assert fmts == [orc.FMT_NVFP4]
 
 
-def test_tdc_host_matches_oracle(L, orc):
+@pytest.mark.parametrize("metric", ["cos", "rel_l2"])
+def test_tdc_host_matches_oracle(L, orc, metric):
     from paper_2603_18742_b200 import dmpq
     rng = np.random.default_rng(2)
     for trial in range(300):
-        cfg_o = orc.TdcConfig(rho=float(rng.uniform(0, 0.002)), tau=float(rng.uniform(0, 0.006)),
-                              n_max=int(rng.integers(1, 4)))
-        cfg_c = L.TdcConfig(cfg_o.rho, cfg_o.tau, cfg_o.n_max)
+        cfg_o = orc.TdcConfig(rho=float(rng.uniform(0, 0.002)), tau=float(rng.uniform(0, 0.006)) * (30 if metric != "cos" else 1),
+                              n_max=int(rng.integers(1, 4)), metric=metric)
+        cfg_c = L.TdcConfig(cfg_o.rho, cfg_o.tau, cfg_o.n_max, L.TDC_METRIC_REL_L2 if metric == "rel_l2" else L.TDC_METRIC_COS)
         so, sc = orc.TdcState(), dmpq.tdc_new_state()
         for t in range(30):
             do = orc.tdc_decide(so, cfg_o, t)
@@ -111,7 +112,7 @@ def test_tdc_host_matches_oracle(L, orc):
             # synthetic stats whose cosine error straddles tau
             cos = 1.0 - float(rng.uniform(0, 0.006))
             st = [0, 1, 0, 1, cos, 1.0, 1.0]
-            e = orc.cosine_error_from_stats(st[4], st[5], st[6])
+            e = orc.prediction_error_from_stats(st, metric)
             orc.tdc_update(so, cfg_o, t, do, e)
             dmpq.tdc_update(sc, cfg_c, t, dc, st)
             assert sc.e_acc == so.e_acc and sc.t_p == so.t_p

@@ -56,6 +56,9 @@ MODES = {
     # producer-fused NVFP4 quantization of the FFN2 input in FFN1's epilogue (NEXT-2; plain quantizer);
     # tau_gamma scaled so that the FFN2 layer routes NVFP4 on some steps
     "dmpq_fused_quant": (False, False, 25.0, False, 0.02, False, False, False, True),
+    # the "current" NVFP4 global scale (R3 variant: amax pass over this input, g = amax / 2688) and the
+    # relative-L2 distance of Eq. 9 (R19)
+    "hadamard_g_current_rel_l2": (True, False, 25.0, False, 0.1, False, False, False, False, "current", "rel_l2"),
 }
 
 
@@ -80,10 +83,12 @@ def run(request):
     cast = len(MODES[request.param]) > 6 and MODES[request.param][6]
     i8b = len(MODES[request.param]) > 7 and MODES[request.param][7]
     fq = len(MODES[request.param]) > 8 and MODES[request.param][8]
+    gpol = MODES[request.param][9] if len(MODES[request.param]) > 9 else "delayed"
+    tmetric = MODES[request.param][10] if len(MODES[request.param]) > 10 else "cos"
     # gates chosen so Gamma straddles the per-layer thresholds (mixed NVFP4 / INT8)
     stack = DiTStack(1, H, F, M, dev, seed=3, gate_scales=[0.008], hadamard=had, pdr=pdr, tau_outlier=tau_o,
-                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2), fuse_refresh=fused, int8_cast=cast, int8_block=i8b, fuse_quant=fq,
-                     tau_gamma=[0.05] * 6 if fq else None)
+                     cache_nvfp4=c4, tdc_cfg=(0.001, tau_c, 2, 1 if tmetric == "rel_l2" else 0), fuse_refresh=fused,
+                     int8_cast=cast, int8_block=i8b, fuse_quant=fq, tau_gamma=[0.05] * 6 if fq else None, g_policy=gpol)
     A, B = synth.trajectory_basis(M, H, seed=77)
     steps = []
     for t in range(T):
@@ -168,6 +173,9 @@ def test_stages_teacher_forced(run, orc):
         qs = {}
         for f_ in set(fm[0:3]):
             qs[f_] = _check_quant(orc, cap["h1"], cap.get("a0_i8" if f_ == D.FMT_INT8 else "a0_f4"), f_, H, had)
+        if stack.g_policy == "current" and D.FMT_NVFP4 in fm[0:3]:   # g from this input's own amax (R3)
+            y = orc.fht128(orc.bf16_to_f32(bits(cap["h1"])).reshape(-1, H)) if had else f32(cap["h1"])
+            assert float(cap["a0_f4"]["g"].item()) == orc.global_scale(float(np.abs(y).max()), 2688.0)
         for j in range(3):
             ref, exact = _gemm_ref(orc, fm[j], qs[fm[j]], W.layers[j], H, H)
             if exact:
@@ -235,7 +243,8 @@ def test_decisions_match_oracle(run, orc):
     """Routing (Eq. 7 + fallbacks) and TDC (Eqs. 10-11) from the GPU statistics equal
     the oracle's decisions step by step (exemption: within 1e-6 of a threshold)."""
     stack, steps = run
-    cfg = orc.TdcConfig(rho=stack.cfg.rho, tau=stack.cfg.tau, n_max=stack.cfg.n_max)
+    metric = "rel_l2" if stack.cfg.metric == 1 else "cos"
+    cfg = orc.TdcConfig(rho=stack.cfg.rho, tau=stack.cfg.tau, n_max=stack.cfg.n_max, metric=metric)
     s = orc.TdcState()
     prev_stats, prev_skipped = None, False
     mixed = set()
@@ -264,7 +273,7 @@ def test_decisions_match_oracle(run, orc):
                     continue
                 assert a == b, (t, j, gamma, stack.tau[j])
             mixed.update(st["fmts"])
-            e = orc.cosine_error_from_stats(st["stats"][4], st["stats"][5], st["stats"][6])  # [7:] = PDR sums
+            e = orc.prediction_error_from_stats(st["stats"], metric)  # [7:] = PDR sums
             orc.tdc_update(s, cfg, t, 0, e)
             prev_stats, prev_skipped = st["stats"], False
         else:

@@ -803,3 +803,27 @@ def test_gemm_int8_blocks_exact_fractions(orc):
     acc = a.astype(np.int64) @ w.astype(np.int64).T
     ref = acc.astype(np.float64) * sa[:, :1].astype(np.float64) * sw.astype(np.float64)[None, :]
     np.testing.assert_allclose(y_eq, ref, rtol=1e-15)
+
+
+def test_rel_l2_prediction_error(orc):
+    """Eq. 9 with D = relative-L2 distance (R19) from the refresh statistics: SPEC rel_l2
+    examples with Delta_prev as the reference, numpy's norm of the difference on random
+    deltas, zero reference -> +inf; and it differs from 1 - cos where it should."""
+    z = bf16_bits(np.zeros(2, np.float32))
+    for dn, dp, want in (([0.0, 0.0], [3.0, 4.0], 1.0), ([0.0, 1.0], [1.0, 0.0], math.sqrt(2.0)),
+                         ([2.0, 2.0], [1.0, 1.0], 1.0), ([1.5, -0.5], [1.5, -0.5], 0.0)):
+        _, st = orc.block_stats(z, bf16_bits(dn), bf16_bits(dp))
+        assert orc.prediction_error_from_stats(st, "rel_l2") == pytest.approx(want, abs=1e-15)
+    _, st = orc.block_stats(z, bf16_bits([2.0, 2.0]), bf16_bits([1.0, 1.0]))
+    assert orc.prediction_error_from_stats(st, "cos") == pytest.approx(0.0, abs=1e-15)   # scaled: cos blind
+    _, st = orc.block_stats(z, bf16_bits([1.0, 1.0]), bf16_bits([0.0, 0.0]))
+    assert orc.prediction_error_from_stats(st, "rel_l2") == math.inf
+    rng = np.random.default_rng(33)
+    n = 4096
+    xi = bf16_bits(rng.standard_normal(n).astype(np.float32))
+    xo = bf16_bits((bf16_vals(xi) + 0.05 * rng.standard_normal(n)).astype(np.float32))
+    dp = bf16_bits((0.05 * rng.standard_normal(n)).astype(np.float32))
+    dn, st = orc.block_stats(xi, xo, dp)
+    a, b = bf16_vals(dn).astype(np.float64), bf16_vals(dp).astype(np.float64)
+    assert orc.prediction_error_from_stats(st, "rel_l2") == pytest.approx(np.linalg.norm(a - b) / np.linalg.norm(b),
+                                                                          rel=1e-12)
