@@ -90,10 +90,16 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8
 #endif
 constexpr int EPI_WARPS = DMPQ_EPI_WARPS;   // epilogue warps per CTA (2 per TMEM lane quarter, column-interleaved)
 #ifndef DMPQ_GEMM_PREFETCH
-#define DMPQ_GEMM_PREFETCH 0   // L2 prefetch of the next tile's A / B rows at the start of each tile (measured 25-30 % slower)
+#define DMPQ_GEMM_PREFETCH 0   // 1: L2 prefetch of the next tile's A / B rows at each tile start (measured 25-30 % slower);
+                               // 2: the next tile's A, one K block per K block (~8 % slower). A partitioned prefetch (each
+                               // pair its 1/num_n_tiles share of the next A panel, fetched once from DRAM) was no faster
+                               // at K = 3072 and 1-5 % slower at K = 12288 (round 2): DRAM latency is not the tile-start limiter
 #endif
 #ifndef DMPQ_MAX_STAGING
 #define DMPQ_MAX_STAGING 3     // output/residual staging buffers per epilogue warp (at most)
+#endif
+#ifndef DMPQ_EPI_PAIR
+#define DMPQ_EPI_PAIR 1        // 1: the two epilogue warps of a TMEM lane quarter share 32 x 64-column staging buffers (128-B rows, one TMA store / residual load per chunk pair)
 #endif
 #ifndef DMPQ_GEMM_RASTER
 #define DMPQ_GEMM_RASTER 0     // 0: pair c takes tiles c, c + P, ... (n-fastest); 1: a contiguous run of tiles per pair
@@ -129,6 +135,8 @@ struct PairLayout {
         (DMPQ_MAX_STAGING >= 3 && STAGING_OFFSET + EPI_WARPS * 3 * 2048 + VEC_BYTES + 512 + 1024 <= SMEM_LIMIT) ? 3
         : (STAGING_OFFSET + EPI_WARPS * 2 * 2048 + VEC_BYTES + 512 + 1024 <= SMEM_LIMIT) ? 2 : 1;
     static constexpr int STAGING_BYTES = EPI_WARPS * STAGING_BUFS * 2048;
+    // DMPQ_EPI_PAIR: the two warps of a lane quarter share 128-B-row staging buffers (needs >= 2 of them)
+    static constexpr bool PAIRED = DMPQ_EPI_PAIR != 0 && EPI_WARPS == 8 && STAGING_BUFS >= 2;
     static constexpr int VEC_OFFSET = STAGING_OFFSET + STAGING_BYTES;
     static constexpr int BAR_OFFSET = VEC_OFFSET + VEC_BYTES;
     static constexpr int TOTAL = BAR_OFFSET + 512 + 1024;   // mbarriers, TMEM holder, residual barriers
@@ -324,7 +332,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         }
         else if constexpr (!I8) gg = 1.0f;   // BF16: y = fma(acc, 1, bias) = fl(acc + bias)
         const f2 gg2 = f2make(gg, gg);
-        const uint32_t staging = sbase + L::STAGING_OFFSET + ew * (L::STAGING_BUFS * 2048);
+        // staging: per warp NSB x (32 rows x 64 B, 64-B swizzle), or (DMPQ_EPI_PAIR) per lane quarter
+        // NSB x (32 rows x 128 B, 128-B swizzle), warp chalf owning bytes [64 chalf, 64 chalf + 64) of a row
+        constexpr bool PAIRST = L::PAIRED;
+        constexpr uint32_t SBUF = PAIRST ? 4096 : 2048;
+        const uint32_t staging = PAIRST ? sbase + L::STAGING_OFFSET + q * (L::STAGING_BUFS * 4096)
+                                        : sbase + L::STAGING_OFFSET + ew * (L::STAGING_BUFS * 2048);
+        const int sb_id = PAIRST ? q : ew;        // residual barrier group
+        const bool issuer = !PAIRST || chalf == 0; // the warp that issues the pair's TMA loads / stores
         const uint32_t vec_s = sbase + L::VEC_OFFSET;
         const bool has_bias = (p.flags & DMPQ_EP_BIAS) != 0;
         const bool has_gelu = (p.flags & DMPQ_EP_GELU_TANH) != 0;
@@ -378,20 +393,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
             const int nch_here = (n_here + 31) >> 5;
             const int my_last = nch_here > chalf ? chalf + ((nch_here - 1 - chalf) / CSTEP) * CSTEP : -1;
             const int nmine = my_last < 0 ? 0 : (my_last - chalf) / CSTEP + 1;   // this warp's chunks of the tile
+            // staging iterations of the tile: one per chunk of this warp, or (paired) one per chunk pair
+            const int niter = PAIRST ? (nch_here + 1) >> 1 : nmine;
             constexpr int NSB = L::STAGING_BUFS;
             // residual chunk j of this warp -> staging buffer (chunk_ctr + j) % NSB, by TMA; the first
             // NSB chunks are requested now, while the mainloop of this tile still runs
             const uint32_t ctr0 = chunk_ctr;   // this tile's first chunk counter
             auto res_load = [&](int j) {
                 const uint32_t cj = ctr0 + (uint32_t)j;
-                mbar_arrive_expect_tx(bar_res + 8 * (ew * 3 + (int)(cj % NSB)), 2048);
-                tma_load_2d(staging + (cj % NSB) * 2048, &tmR, n0 + (chalf + j * CSTEP) * 32, rowbase,
-                            bar_res + 8 * (ew * 3 + (int)(cj % NSB)));
+                mbar_arrive_expect_tx(bar_res + 8 * (sb_id * 3 + (int)(cj % NSB)), SBUF);
+                tma_load_2d(staging + (cj % NSB) * SBUF, &tmR, PAIRST ? n0 + j * 64 : n0 + (chalf + j * CSTEP) * 32, rowbase,
+                            bar_res + 8 * (sb_id * 3 + (int)(cj % NSB)));
             };
-            if (tma_res && nmine > 0) {
+            if (tma_res && niter > 0 && issuer) {
                 if (lane == 0) {
                     bulk_wait_read0();   // every earlier store of this warp has read its staging buffer
-                    for (int j = 0; j < NSB && j < nmine; ++j) res_load(j);
+                    for (int j = 0; j < NSB && j < niter; ++j) res_load(j);
                 }
                 __syncwarp();
             }
@@ -402,11 +419,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(leader_addr(bar_tempty + 8 * acc));
             }
-            for (int c = chalf; c < nch_here; c += CSTEP) {
-                const int jc = (c - chalf) / CSTEP;   // this warp's chunk index in the tile
-                const uint32_t buf = staging + (chunk_ctr % NSB) * 2048;
-                const uint32_t rbar = bar_res + 8 * (ew * 3 + (int)(chunk_ctr % NSB));
+            for (int jc = 0; jc < niter; ++jc) {   // jc: staging iteration of the tile
+                const int c = chalf + jc * CSTEP;      // this warp's chunk (paired: none past the tile's last)
+                const uint32_t buf = staging + (chunk_ctr % NSB) * SBUF;
+                const uint32_t rbar = bar_res + 8 * (sb_id * 3 + (int)(chunk_ctr % NSB));
                 const uint32_t rphase = (chunk_ctr / NSB) & 1;
+                // this lane's 16-byte piece v4 (0..3) of its row in the staging buffer
+                auto sptr = [&](int v4) -> uint32_t {
+                    return PAIRST ? buf + lane * 128 + (((uint32_t)(chalf * 4 + v4) ^ (lane & 7)) << 4)      // 128B swizzle
+                                  : buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);             // 64B swizzle
+                };
+                if (c < nch_here) {
                 // gated-residual chunk (TMA-staged: requested ahead, see res_load; else loaded
                 // here, before the TMEM read so the two latencies overlap)
                 uint4 rv4[4];
@@ -473,7 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     mbar_wait(rbar, rphase);
 #pragma unroll
                     for (int v4 = 0; v4 < 4; ++v4) {
-                        const uint32_t a = buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);
+                        const uint32_t a = sptr(v4);
                         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                                      : "=r"(rv4[v4].x), "=r"(rv4[v4].y), "=r"(rv4[v4].z), "=r"(rv4[v4].w) : "r"(a) : "memory");
                     }
@@ -530,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     }
                 }
                 if (p.Y) {
-                    if (!tma_res) {
+                    if (!tma_res && !PAIRST) {
                         if (lane == 0) {   // the store issued from this buffer (2 chunks ago / last chunk) has read it
                             if constexpr (L::STAGING_BUFS == 3) bulk_wait_read2();
                             else if constexpr (L::STAGING_BUFS == 2) bulk_wait_read1();
@@ -539,23 +562,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                         __syncwarp();
                     }
 #pragma unroll
-                    for (int v4 = 0; v4 < 4; ++v4) {
-                        const uint32_t a = buf + lane * 64 + (((uint32_t)v4 ^ ((lane >> 1) & 3)) << 4);  // 64B swizzle
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(yb[4 * v4]),
+                    for (int v4 = 0; v4 < 4; ++v4)
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sptr(v4)), "r"(yb[4 * v4]),
                                      "r"(yb[4 * v4 + 1]), "r"(yb[4 * v4 + 2]), "r"(yb[4 * v4 + 3])
                                      : "memory");
-                    }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {
-                            tma_store_2d(&tmY, buf, col0, rowbase);
+                    if (!PAIRST && lane == 0) {
+                        tma_store_2d(&tmY, buf, col0, rowbase);
                         bulk_commit();
                         if (tma_res && jc + NSB < nmine) {   // this buffer's next residual chunk, once the store has read it
                             bulk_wait_read0();
                             res_load(jc + NSB);
                         }
                     }
-                    ++chunk_ctr;
                 }
                 if (has_tdc && row_ok) {
                     // TDC refresh (Eq. 8) with tdc_step's arithmetic: d = fl(X_out - X_in),
@@ -606,6 +626,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                                 ap[v4] = make_int4((int)r[4 * v4], (int)r[4 * v4 + 1], (int)r[4 * v4 + 2], (int)r[4 * v4 + 3]);
                         }
                     }
+                }
+                }   // c < nch_here
+                if (p.Y) {
+                    if constexpr (PAIRST) {
+                        // both halves written: one TMA store of the 32 x 64 box. Without a TMA-staged
+                        // residual the issuer first lets the store NSB - 1 iterations back finish reading
+                        // its buffer, so this barrier also frees the next iteration's buffer.
+                        if (!tma_res && issuer && lane == 0) {
+                            if constexpr (L::STAGING_BUFS == 3) bulk_wait_read1();
+                            else bulk_wait_read0();
+                        }
+                        named_bar_sync(2 + q, 64);
+                        if (issuer && lane == 0) {
+                            tma_store_2d(&tmY, buf, n0 + jc * 64, rowbase);
+                            bulk_commit();
+                            if (tma_res && jc + NSB < niter) {   // this buffer's next residual chunk pair
+                                bulk_wait_read0();
+                                res_load(jc + NSB);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    ++chunk_ctr;
                 }
             }
         }
@@ -898,16 +941,18 @@ static bool make_tmap_sf(CUtensorMap* tm, const void* base, int row_tiles, int k
     return r == CUDA_SUCCESS;
 }
 
-// bf16 output [rows x cols] (row stride ld elements), box 32 x 32, 64-B swizzle (epilogue TMA store).
-static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, int ld) {
+// bf16 output [rows x cols] (row stride ld elements), box 32 x 32 with 64-B swizzle, or (wide, paired
+// epilogue staging) 32 rows x 64 columns with 128-B swizzle (epilogue TMA store / residual load).
+static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, int ld, bool wide) {
     auto enc = tmap_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {32, 32};
+    cuuint32_t box[2] = {wide ? 64u : 32u, 32};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -937,9 +982,9 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
             !make_tmap_sf(&tmSFB, p.sfb, p.sfb_row_tiles, p.kc4, 2))
             return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (scales)");
     }
-    if (p.Y && !make_tmap_y(&tmY, p.Y, p.m, p.n, p.ldy))
+    if (p.Y && !make_tmap_y(&tmY, p.Y, p.m, p.n, p.ldy, L::PAIRED))
         return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (Y)");
-    if (p.Y && (p.flags & DMPQ_EP_RESIDUAL) && !make_tmap_y(&tmR, p.residual, p.m, p.n, p.ldr))
+    if (p.Y && (p.flags & DMPQ_EP_RESIDUAL) && !make_tmap_y(&tmR, p.residual, p.m, p.n, p.ldr, L::PAIRED))
         return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (residual)");
     p.num_m_tiles = (p.m + 255) / 256;
     p.num_n_tiles = (p.n + BN - 1) / BN;

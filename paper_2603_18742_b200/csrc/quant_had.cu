@@ -55,6 +55,20 @@ __device__ __forceinline__ float rtab_lookup(uint32_t a) {
 }
 __device__ __forceinline__ f2 habs2(f2 a) { f2 r; r.v = a.v & 0x7FFFFFFF7FFFFFFFull; return r; }
 
+#ifndef DMPQ_HAD_S1_MIXED
+#define DMPQ_HAD_S1_MIXED 0   // experiment: plain variant's FHT stage 1 by the mixed bf16/fp32 add + FMA on load
+#endif
+// FHT stage h = 1 (R14) of the bf16 pair w = [b:a], straight from the packed word:
+// (fl(a + b), fl(a - b)) by the sm_100 mixed-precision add / FMA (FHADD.BF16 / FHFMA.BF16:
+// bf16 operand, fp32 operand and result, one rounding; b * -1 is exact).
+__device__ __forceinline__ f2 had_stage1_bf16x2(uint32_t w) {
+    float s, d;
+    asm("{\n\t.reg .b16 lo, hi, m1;\n\t.reg .f32 a;\n\tmov.b32 {lo, hi}, %2;\n\tmov.b16 m1, 0xBF80;\n\t"
+        "shl.b32 a, %2, 16;\n\tadd.rn.f32.bf16 %0, hi, a;\n\tfma.rn.f32.bf16 %1, hi, m1, a;\n\t}"
+        : "=f"(s), "=f"(d) : "r"(w));
+    return f2make(s, d);
+}
+
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, int x, int y, int z, int w, uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
@@ -225,22 +239,24 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
         mbar_wait(bar0 + 8 * b, ph);
         const uint32_t buf = sbase + b * set_stride;
 
+        constexpr bool S1_ON_LOAD = DMPQ_HAD_S1_MIXED && !LN && !PDR;
+        auto unpack = [](uint32_t w) { return S1_ON_LOAD ? had_stage1_bf16x2(w) : bf16x2_to_f2(w); };
         f2 Y[64];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint4 v = hlds128((buf + x0) ^ (u << 4));
-            Y[4 * u] = bf16x2_to_f2(v.x);
-            Y[4 * u + 1] = bf16x2_to_f2(v.y);
-            Y[4 * u + 2] = bf16x2_to_f2(v.z);
-            Y[4 * u + 3] = bf16x2_to_f2(v.w);
+            Y[4 * u] = unpack(v.x);
+            Y[4 * u + 1] = unpack(v.y);
+            Y[4 * u + 2] = unpack(v.z);
+            Y[4 * u + 3] = unpack(v.w);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint4 v = hlds128((buf + x1) ^ (u << 4));
-            Y[32 + 4 * u] = bf16x2_to_f2(v.x);
-            Y[32 + 4 * u + 1] = bf16x2_to_f2(v.y);
-            Y[32 + 4 * u + 2] = bf16x2_to_f2(v.z);
-            Y[32 + 4 * u + 3] = bf16x2_to_f2(v.w);
+            Y[32 + 4 * u] = unpack(v.x);
+            Y[32 + 4 * u + 1] = unpack(v.y);
+            Y[32 + 4 * u + 2] = unpack(v.z);
+            Y[32 + 4 * u + 3] = unpack(v.w);
         }
 
         if constexpr (LN) {
@@ -308,12 +324,13 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
                 const float rsum = sr.sum(cvalid ? __fadd_rn(f2lo(sa), f2hi(sa)) : 0.0f, s0 + 3);
                 if (t == 0 && row_live && p.row_abs_sum) p.row_abs_sum[row] = rsum;
             }
-            // FHT stage h = 1 inside each pair (R14)
-            const f2 pm = f2make(1.0f, -1.0f);
+            if constexpr (!S1_ON_LOAD) {   // FHT stage h = 1 inside each pair (R14)
+                const f2 pm = f2make(1.0f, -1.0f);
 #pragma unroll
-            for (int q = 0; q < 64; ++q) {
-                const float a = f2lo(Y[q]), bb = f2hi(Y[q]);
-                Y[q] = fma2(f2make(bb, bb), pm, f2make(a, a));
+                for (int q = 0; q < 64; ++q) {
+                    const float a = f2lo(Y[q]), bb = f2hi(Y[q]);
+                    Y[q] = fma2(f2make(bb, bb), pm, f2make(a, a));
+                }
             }
         }
 

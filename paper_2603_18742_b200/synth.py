@@ -63,6 +63,10 @@ def adversarial_rows(k: int) -> torch.Tensor:
     r = torch.randn(k, generator=_gen(7)) * 1e-3; r[0] = 300.0; rows.append(r)   # subnormal-scale blocks
     r = torch.zeros(k); r[0::16] = 0.17578125; r[1::16] = 0.03662109375; rows.append(r)  # R4 tie vector
     r = torch.arange(k, dtype=torch.float32) - k / 2; rows.append(r)
+    # bf16 subnormals (|x| < 2^-126) next to a few small normals that keep the INT8 row scale's
+    # reciprocal finite: sums of subnormals survive into the codes (no flush-to-zero anywhere)
+    r = torch.randn(k, generator=_gen(8)) * 3e-39; r[0::128] = 4e-37; rows.append(r)
+    r = torch.rand(k, generator=_gen(9)) * 1.1e-38; r[5] = -1e-36; rows.append(r)
     # INT8 exact ties: row max 127 -> x * 127/amax = x; k + 0.5 values must round half to even
     r = torch.tensor([127.0, 2.5, 3.5, 0.5, 1.5, -4.5, 126.5, -0.5, -1.5, 5.5, -126.5, 0.0, 64.5, -63.5, 7.5, 8.5])
     rows.append(r.repeat(k // 16))
