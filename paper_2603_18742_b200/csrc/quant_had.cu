@@ -4,9 +4,12 @@
 // and the PDR input statistics (R15).
 //
 // Layout. One thread owns one whole 128-element Hadamard block (two 128-byte lines), so all
-// seven FHT stages run in registers with no lane exchange: stage h = 1 is one FFMA2 per pair
-// (fl(b * (+1, -1) + a) = (fl(a + b), fl(a - b)), the exact product leaves one rounding),
-// stages h = 2..64 are packed FADD2 butterflies between register pairs — the oracle's fixed
+// seven FHT stages run in registers with no lane exchange: stage h = 1 is formed straight from
+// the loaded bf16 word by the mixed-precision FHADD.BF16 / FHFMA.BF16 (plain variant; three
+// instructions per pair, measured -3.5 % quantizer time in the CogVideoX-5B step) or, after
+// LN / the PDR statistics, one FFMA2 per pair (fl(b * (+1, -1) + a) = (fl(a + b), fl(a - b)),
+// the exact product leaves one rounding); stages h = 2..64 are packed FADD2 butterflies between
+// register pairs — the oracle's fixed
 // butterfly order (R14), so codes are bit-exact. A CTA owns R rows at a time ("row set"),
 // tpr threads per row (thread t = block t; tpr = blocks per row rounded up to 8, or to 32
 // above 32). Rows arrive by TMA into a 2-4 deep shared-memory ring with full/empty mbarriers.
@@ -56,7 +59,7 @@ __device__ __forceinline__ float rtab_lookup(uint32_t a) {
 __device__ __forceinline__ f2 habs2(f2 a) { f2 r; r.v = a.v & 0x7FFFFFFF7FFFFFFFull; return r; }
 
 #ifndef DMPQ_HAD_S1_MIXED
-#define DMPQ_HAD_S1_MIXED 0   // experiment: plain variant's FHT stage 1 by the mixed bf16/fp32 add + FMA on load
+#define DMPQ_HAD_S1_MIXED 1   // plain variant: FHT stage 1 by the mixed bf16/fp32 add + FMA on load (0: unpack + FFMA2)
 #endif
 // FHT stage h = 1 (R14) of the bf16 pair w = [b:a], straight from the packed word:
 // (fl(a + b), fl(a - b)) by the sm_100 mixed-precision add / FMA (FHADD.BF16 / FHFMA.BF16:
@@ -350,8 +353,12 @@ __global__ void __launch_bounds__(HT_MAX, LN ? DMPQ_HAD_LN_MINB : 3) quant_had_k
 
         // the row set is in registers: release buffer b and (thread 0, once every warp has
         // released it) refill it with row set it + nbuf, so nbuf row sets stay in flight.
-        // (Releasing right after the shared-memory loads was measured 2-5 % slower and let a
-        // TMA refill race the loads' completion: a rare wrong row in the dense-row test.)
+        // The proxy fence orders this thread's generic-proxy shared loads before the TMA
+        // (async-proxy) refill that the release allows: the compiler hoists the arrive above
+        // the transform (it is pure register work), and without the fence the arrive does not
+        // wait for loads still in flight — a schedule with the arrive five instructions after
+        // the last load lost whole 128-blocks to the refill (~3 in 10^4 blocks, dense-row test).
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8 * (nbuf + b));
         if (tid == 0 && it + nbuf < iters) {
