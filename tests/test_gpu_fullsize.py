@@ -314,3 +314,39 @@ def test_max_size_hunyuan_rows_sampled(D, orc):
         got = y4[r].float().cpu().numpy().astype(np.float64)
         assert np.linalg.norm(got - yr4[0]) <= 4e-3 * np.linalg.norm(yr4[0]), r
     assert amax.item() >= ymax
+
+
+@pytest.mark.parametrize("k,ln,which", [(12288, False, "int8"), (3072, False, "int8"), (3072, True, "int8"),
+                                        (3072, False, "nvfp4"), (3072, True, "nvfp4")])
+def test_fullsize_hadamard_dense_all_rows(D, orc, k, ln, which):
+    """Every row, every code of the bench's Hadamard quantizer launches at full size (M = 35,552:
+    15-60 row sets per CTA through the TMA ring), three launches on different inputs, against the
+    oracle: a guard against rare shared-memory reuse races (round-2b: a TMA refill
+    overtaking shared loads lost whole 128-blocks ~3 times in 10^4), which sampled rows would miss.
+    LN variants: the h-writing launch gives the LN rows, the bench's launch (no h) the codes."""
+    g = torch.tensor([0.02], device="cuda")
+    for rep in range(3):
+        xd = synth.dit_activation_device(M, k, 31 + rep, "cuda")
+        if k != 3072:   # FFN2 input: GELU-tanh of an FFN1-like tensor (synth.ffn2_activation's recipe)
+            xd = torch.nn.functional.gelu(xd.float(), approximate="tanh").to(torch.bfloat16)
+        x = xd.cpu()
+        h = None
+        if ln:
+            h = torch.empty(M, k, dtype=torch.bfloat16, device="cuda")
+            D.dmpq_quantize_act(xd, out_i8=D.QuantAct.empty(D.FMT_INT8, M, k, "cuda"), layernorm=True, h_out=h,
+                                hadamard=True)
+        a = D.QuantAct.empty(D.FMT_INT8 if which == "int8" else D.FMT_NVFP4, M, k, "cuda",
+                             g=g if which == "nvfp4" else None)
+        D.dmpq_quantize_act(xd, out_i8=a if which == "int8" else None, out_fp4=a if which == "nvfp4" else None,
+                            layernorm=ln, hadamard=True)
+        torch.cuda.synchronize()
+        y = orc.fht128(orc.bf16_to_f32(synth.bits(h.cpu() if ln else x)).reshape(M, k))
+        if which == "int8":
+            c8, s8 = orc.int8_quantize_f32(y)
+            assert np.array_equal(a.row_scale.cpu().numpy(), s8), rep
+            bad = np.argwhere(a.codes.cpu().numpy() != c8)
+        else:
+            c4, s4 = orc.nvfp4_quantize_f32(y, 0.02)
+            assert np.array_equal(orc.sf_unswizzle(a.sf.cpu().numpy(), M, k), s4), rep
+            bad = np.argwhere(a.codes.cpu().numpy() != c4)
+        assert len(bad) == 0, f"launch {rep}: {len(bad)} codes differ, first at {bad[:4].tolist()}"
