@@ -144,8 +144,13 @@ struct PairLayout {
     static_assert(TOTAL <= SMEM_LIMIT, "shared memory budget");
 };
 
-template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false>   // TDC: fused refresh; QNT: fused NVFP4 quantizer
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS, 1)
+// CL = 2: one CTA pair per cluster. CL = 4 (experiment, DMPQ_GEMM_CLUSTER=4): two pairs per cluster
+// work on vertically adjacent 256-row tiles of the same N tile; each CTA loads a quarter of the
+// pair's B tile and TMA-multicasts it to the same-rank CTA of the other pair, and two CTAs load the
+// NVFP4 SFB atoms for all four (B and SFB L2 reads halved / quartered); a stage is refilled only
+// once both pairs' MMAs have released it.
+template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false, int CL = 2>   // TDC: fused refresh; QNT: fused NVFP4 quantizer
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS, 1)
     dmpq_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
@@ -167,7 +172,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     const uint32_t bar_res = bar_full + 2 * STAGES * 8 + 4 * 8 + 16;   // [EPI_WARPS][3] residual-chunk TMA loads
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
+    static_assert(CL == 2 || CL == 4, "cluster of one or two CTA pairs");
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1;            // rank inside the CTA pair
+    const int pp = (int)(crank >> 1);           // pair index inside the cluster (CL = 4)
+    constexpr uint16_t EMPTY_MASK = CL == 4 ? 0xF : 0x3;
+    const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pp));
     // accumulator buffers in TMEM: two (the epilogue of tile i overlaps the mainloop of tile
     // i + 1) unless BN = 256 NVFP4, where 2 x 256 columns leave no room for the scale factors:
     // one buffer, and the mainloop of tile i + 1 waits for the epilogue of tile i
@@ -185,7 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         if (p.Y && (p.flags & DMPQ_EP_RESIDUAL)) prefetch_tmap(&tmR);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, CL / 2);   // every pair that reads the stage releases it
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(bar_tfull + 8 * a, 1);
@@ -199,7 +209,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int num_tiles = p.num_m_tiles * p.num_n_tiles;   // pair tiles (256 rows each)
+    // cluster tiles: CL = 2 one 256-row pair tile, CL = 4 a 512-row group (pair pp takes its half)
+    const int num_mg = CL == 4 ? (p.num_m_tiles + 1) >> 1 : p.num_m_tiles;
+    const int num_tiles = num_mg * p.num_n_tiles;
+    auto tile_mt = [&](int tile) { return CL == 4 ? (tile / p.num_n_tiles) * 2 + pp : tile / p.num_n_tiles; };
     const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
     int ts0, ts1, tstep;
     tile_span(cid, ncl, num_tiles, ts0, ts1, tstep);
@@ -209,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         int stage = 0;
         uint32_t phase = 0;
         for (int tile = ts0; tile < ts1; tile += tstep) {
-            const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
+            const int mt = tile_mt(tile), nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int m0 = mt * 256 + (int)rank * BM;
             const int nb0 = nt * BN + (int)rank * (BN / 2);
             // next tile's A rows, one K block per K block of this tile (mode 2)
@@ -237,13 +250,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                     const uint32_t sA = sbase + stage * L::STAGE_BYTES;
                     const uint32_t sB = sA + L::A_BYTES;
                     tma_load_2d_pair(sA, &tmA, kb * BK_BYTES, m0, full_l);
-                    tma_load_2d_pair(sB, &tmB, kb * BK_BYTES, nb0, full_l);
+                    if constexpr (CL == 4) {   // quarter pp of this CTA's B half -> both pairs' same-rank CTAs
+                        tma_load_2d_pair_mc(sB + pp * (BN / 4) * BK_BYTES, &tmB, kb * BK_BYTES, nb0 + pp * (BN / 4), full_l,
+                                            (uint16_t)((1u << rank) | (1u << (rank + 2))));
+                    } else {
+                        tma_load_2d_pair(sB, &tmB, kb * BK_BYTES, nb0, full_l);
+                    }
                     if (pf2 && pf_m != m0) tma_prefetch_2d(&tmA, kb * BK_BYTES, pf_m);
                     if constexpr (FP4) {
                         const uint32_t sSFA = sB + L::B_BYTES;
                         const uint32_t sSFB = sSFA + L::SFA_BYTES;
                         tma_load_3d_pair(sSFA, &tmSFA, 0, kb * 4, mt * 2 + (int)rank, full_l);
-                        tma_load_3d_pair(sSFB, &tmSFB, 0, kb * 4, (nt * BN) >> 7, full_l);
+                        if constexpr (CL == 4) {   // CTAs 0 / 1 load SFB row tile 0 / 1 for all four
+                            if (crank < 2)
+                                tma_load_3d_pair_mc(sSFB + crank * 2048, &tmSFB, 0, kb * 4, ((nt * BN) >> 7) + (int)crank, full_l, 0xF);
+                        } else {
+                            tma_load_3d_pair(sSFB, &tmSFB, 0, kb * 4, (nt * BN) >> 7, full_l);
+                        }
                     }
                 }
                 __syncwarp();
@@ -302,12 +325,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
                             else
                                 mma_f16_pair(d_t, adesc + 2 * j, bdesc + 2 * j, idesc, accum);
                         }
-                        tc_commit_pair_mc(bar_empty + 8 * stage, 0x3);
+                        tc_commit_pair_mc(bar_empty + 8 * stage, EMPTY_MASK);
                     }
                     __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (elect_one()) tc_commit_pair_mc(bar_tfull + 8 * acc, 0x3);
+                if (elect_one()) tc_commit_pair_mc(bar_tfull + 8 * acc, pair_mask);
                 __syncwarp();
             }
         }
@@ -355,7 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI_WARPS
         const float qg = QNT ? *p.q_g : 1.0f;   // the consumer's NVFP4 global scale (R3)
         float qamax = 0.0f;
         for (int tile = ts0; tile < ts1; tile += tstep, ++local) {
-            const int mt = tile / p.num_n_tiles, nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
+            const int mt = tile_mt(tile), nt = tile % p.num_n_tiles;   // n-fastest: A tile reused across N while L2-resident
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int n0 = nt * BN;
@@ -957,16 +980,16 @@ static bool make_tmap_y(CUtensorMap* tm, const void* base, int rows, int cols, i
     return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false>
+template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false, int CL = 2>
 static dmpq_status set_pair_attrs() {
     using L = PairLayout<KIND, BN, STAGES>;
-    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC, QNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC, QNT, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              L::TOTAL) != cudaSuccess)
         return check_launch("dmpq_gemm(smem attribute)");
     return DMPQ_OK;
 }
 
-template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false>
+template <int KIND, int BN, int STAGES, bool TDC = false, bool QNT = false, int CL = 2>
 static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const void* w_codes, cudaStream_t s) {
     using L = PairLayout<KIND, BN, STAGES>;
     constexpr bool FP4 = KIND == 1;
@@ -975,11 +998,11 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     std::memset(&tmSFB, 0, sizeof(tmSFB));
     std::memset(&tmY, 0, sizeof(tmY));
     std::memset(&tmR, 0, sizeof(tmR));
-    if (!make_tmap(&tmA, a_codes, p.m, p.kbytes, BM) || !make_tmap(&tmB, w_codes, p.n, p.kbytes, BN / 2))
+    if (!make_tmap(&tmA, a_codes, p.m, p.kbytes, BM) || !make_tmap(&tmB, w_codes, p.n, p.kbytes, BN / CL))
         return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (A/B)");
     if constexpr (FP4) {
         if (!make_tmap_sf(&tmSFA, p.sfa, (p.m + 127) / 128, p.kc4, 1) ||
-            !make_tmap_sf(&tmSFB, p.sfb, p.sfb_row_tiles, p.kc4, 2))
+            !make_tmap_sf(&tmSFB, p.sfb, p.sfb_row_tiles, p.kc4, CL == 4 ? 1 : 2))
             return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (scales)");
     }
     if (p.Y && !make_tmap_y(&tmY, p.Y, p.m, p.n, p.ldy, L::PAIRED))
@@ -989,17 +1012,33 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
     p.num_m_tiles = (p.m + 255) / 256;
     p.num_n_tiles = (p.n + BN - 1) / BN;
     p.num_kb = (p.kbytes + BK_BYTES - 1) / BK_BYTES;
-    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC, QNT>;
+    auto kern = dmpq_gemm_pair_kernel<KIND, BN, STAGES, TDC, QNT, CL>;
     static bool attr_set = false;   // per process and kernel (dmpq_prepare sets them ahead of graph capture)
     if (!attr_set) {
-        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES, TDC, QNT>();
+        dmpq_status rc = set_pair_attrs<KIND, BN, STAGES, TDC, QNT, CL>();
         if (rc != DMPQ_OK) return rc;
         attr_set = true;
     }
-    const int tiles = p.num_m_tiles * p.num_n_tiles;
-    int clusters = num_sms() / 2;
+    const int tiles = (CL == 4 ? (p.num_m_tiles + 1) / 2 : p.num_m_tiles) * p.num_n_tiles;
+    int clusters = num_sms() / CL;
+    if constexpr (CL == 4) {   // 4-CTA clusters do not tile every GPC: size the persistent grid to what is co-resident
+        static int max_active = 0;
+        if (max_active == 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(CL * clusters);
+            cfg.blockDim = dim3(128 + 32 * EPI_WARPS);
+            cfg.dynamicSmemBytes = L::TOTAL;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+                cudaGetLastError();
+                n = clusters;
+            }
+            max_active = n;
+        }
+        if (clusters > max_active) clusters = max_active;
+    }
     if (clusters > tiles) clusters = tiles;
-    kern<<<2 * clusters, 128 + 32 * EPI_WARPS, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, tmR, p);
+    kern<<<CL * clusters, 128 + 32 * EPI_WARPS, L::TOTAL, s>>>(tmA, tmB, tmSFA, tmSFB, tmY, tmR, p);
     return check_launch("dmpq_gemm");
 }
 
@@ -1029,6 +1068,16 @@ static dmpq_status launch_gemm_i8b(GemmParams p, const void* a_codes, const void
 using namespace dmpq;
 
 // Stage-ring depth of the GEMM (tuning knob, DMPQ_GEMM_STAGES = 5 | 6; default 5: the 6-stage ring only fits with single-buffered output staging, measured slower on the N = 12288 layer).
+// Cluster size of the plain INT8 / NVFP4 GEMMs (experiment knob DMPQ_GEMM_CLUSTER = 2 | 4; 4 = two CTA
+// pairs sharing B / SFB tiles by TMA multicast).
+static int gemm_cluster() {
+    static int c = [] {
+        const char* e = std::getenv("DMPQ_GEMM_CLUSTER");
+        return (e && std::atoi(e) == 4) ? 4 : 2;
+    }();
+    return c;
+}
+
 static int gemm_stages() {
     static int st = [] {
         const char* e = std::getenv("DMPQ_GEMM_STAGES");
@@ -1063,6 +1112,8 @@ extern "C" dmpq_status dmpq_prepare(void) {
         if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 6>();
     }
     if (rc == DMPQ_OK && fp4_bn() == 256) rc = set_pair_attrs<1, 256, 5>();
+    if (rc == DMPQ_OK && gemm_cluster() == 4) rc = set_pair_attrs<1, 192, 5, false, false, 4>();
+    if (rc == DMPQ_OK && gemm_cluster() == 4) rc = set_pair_attrs<0, 256, 5, false, false, 4>();
     if (rc == DMPQ_OK) rc = set_pair_attrs<0, 256, 5, true>();   // fused TDC refresh variants
     if (rc == DMPQ_OK) rc = set_pair_attrs<1, 192, 5, true>();
     if (rc == DMPQ_OK) rc = set_pair_attrs<2, 256, 5, true>();
@@ -1145,6 +1196,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         if (tdc) return launch_gemm_pair<1, 192, 5, true>(p, A->codes, W->fp4_codes, st);
         if (qnt) return launch_gemm_pair<1, 192, 5, false, true>(p, A->codes, W->fp4_codes, st);
         if (fp4_bn() == 256) return launch_gemm_pair<1, 256, 5>(p, A->codes, W->fp4_codes, st);
+        if (gemm_cluster() == 4) return launch_gemm_pair<1, 192, 5, false, false, 4>(p, A->codes, W->fp4_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<1, 192, 5>(p, A->codes, W->fp4_codes, st)
                                  : launch_gemm_pair<1, 192, 6>(p, A->codes, W->fp4_codes, st);
     } else if (A->fmt == DMPQ_FMT_BF16) {
@@ -1168,6 +1220,7 @@ extern "C" dmpq_status dmpq_gemm(const dmpq_act* A, const dmpq_weights* W, const
         }
         if (tdc) return launch_gemm_pair<0, 256, 5, true>(p, A->codes, W->i8_codes, st);
         if (qnt) return launch_gemm_pair<0, 256, 5, false, true>(p, A->codes, W->i8_codes, st);
+        if (gemm_cluster() == 4) return launch_gemm_pair<0, 256, 5, false, false, 4>(p, A->codes, W->i8_codes, st);
         return gemm_stages() == 5 ? launch_gemm_pair<0, 256, 5>(p, A->codes, W->i8_codes, st)
                                  : launch_gemm_pair<0, 256, 6>(p, A->codes, W->i8_codes, st);
     }

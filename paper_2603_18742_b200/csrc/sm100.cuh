@@ -92,6 +92,22 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const void* tmap,
         ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(bar)
         : "memory");
 }
+// Multicast variants: the box lands at the same offset in every CTA of `mask`; each destination's
+// transaction bytes complete on the mbarrier at `bar`'s offset in that CTA's pair leader.
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const void* tmap, int x, int y, uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_mc(uint32_t dst, const void* tmap, int x, int y, int z, uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(bar), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int x, int y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap), "r"(x), "r"(y),
                  "r"(src)
