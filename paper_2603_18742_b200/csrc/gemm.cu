@@ -101,6 +101,9 @@ constexpr int EPI_WARPS = DMPQ_EPI_WARPS;   // epilogue warps per CTA (2 per TME
 #ifndef DMPQ_EPI_PAIR
 #define DMPQ_EPI_PAIR 1        // 1: the two epilogue warps of a TMEM lane quarter share 32 x 64-column staging buffers (128-B rows, one TMA store / residual load per chunk pair)
 #endif
+#ifndef DMPQ_SFB_MC
+#define DMPQ_SFB_MC 1          // NVFP4: the two CTAs of a pair each load one SFB row tile and multicast it to both (SFB L2 reads halved)
+#endif
 #ifndef DMPQ_GEMM_RASTER
 #define DMPQ_GEMM_RASTER 0     // 0: pair c takes tiles c, c + P, ... (n-fastest); 1: a contiguous run of tiles per pair
 #endif
@@ -264,6 +267,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(128 + 32 * EPI_WARP
                         if constexpr (CL == 4) {   // CTAs 0 / 1 load SFB row tile 0 / 1 for all four
                             if (crank < 2)
                                 tma_load_3d_pair_mc(sSFB + crank * 2048, &tmSFB, 0, kb * 4, ((nt * BN) >> 7) + (int)crank, full_l, 0xF);
+                        } else if constexpr (DMPQ_SFB_MC != 0) {   // CTA r loads SFB row tile r for both CTAs of the pair
+                            tma_load_3d_pair_mc(sSFB + rank * 2048, &tmSFB, 0, kb * 4, ((nt * BN) >> 7) + (int)rank, full_l, 0x3);
                         } else {
                             tma_load_3d_pair(sSFB, &tmSFB, 0, kb * 4, (nt * BN) >> 7, full_l);
                         }
@@ -1002,7 +1007,7 @@ static dmpq_status launch_gemm_pair(GemmParams p, const void* a_codes, const voi
         return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (A/B)");
     if constexpr (FP4) {
         if (!make_tmap_sf(&tmSFA, p.sfa, (p.m + 127) / 128, p.kc4, 1) ||
-            !make_tmap_sf(&tmSFB, p.sfb, p.sfb_row_tiles, p.kc4, CL == 4 ? 1 : 2))
+            !make_tmap_sf(&tmSFB, p.sfb, p.sfb_row_tiles, p.kc4, (CL == 4 || DMPQ_SFB_MC) ? 1 : 2))
             return set_error(DMPQ_ECUDA, "dmpq_gemm: cuTensorMapEncodeTiled failed (scales)");
     }
     if (p.Y && !make_tmap_y(&tmY, p.Y, p.m, p.n, p.ldy, L::PAIRED))
