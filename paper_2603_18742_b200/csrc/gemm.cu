@@ -80,9 +80,11 @@ constexpr int BK_BYTES = 128;  // one 128-byte swizzle row per K block (128 int8
 // 256 x BN tile with tcgen05.mma.cta_group::2 (M = 256). Each CTA loads its own
 // 128 A rows and half of the BN B rows (the MMA reads B from both CTAs' smem), so
 // per-SM L2->smem traffic per FLOP drops by 1.5x vs a 1-CTA 128 x BN tile. NVFP4
-// scale atoms arrive by 3-D TMA (OOB -> zero), SFA per CTA, SFB duplicated in both.
+// scale atoms arrive by 3-D TMA (OOB -> zero), SFA per CTA, SFB in both (each CTA loads one
+// row tile and multicasts it to the pair).
 // TMEM: two BN-column accumulators per CTA (epilogue of tile i overlaps the
-// mainloop of tile i+1). Epilogue: TMEM -> registers -> 64B-swizzled smem staging
+// mainloop of tile i+1). Epilogue: TMEM -> registers -> swizzled smem staging (128-B rows shared by
+// the two warps of a lane quarter, DMPQ_EPI_PAIR)
 // -> TMA store; per-column vectors (bias, w_scale, gate) staged in smem per tile.
 // ============================================================================
 #ifndef DMPQ_EPI_WARPS
