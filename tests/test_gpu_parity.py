@@ -771,3 +771,24 @@ def test_gemm_fused_nvfp4_quant(D, orc, fmt, m, n, k, gelu):
     assert np.array_equal(q1.codes.cpu().numpy(), c)
     assert np.array_equal(q1.sf.cpu().numpy(), orc.sf_swizzle(s_, m, n))
     assert am1.item() == orc.amax_bf16(synth.bits(y.cpu()))
+
+
+def test_gemm_cluster4_equals_pairs(tmp_path):
+    """The 4-CTA-cluster option (DMPQ_GEMM_CLUSTER=4: B quarters and SFB atoms shared by TMA multicast
+    between two CTA pairs) gives the CTA-pair GEMMs' outputs bit for bit — same
+    MMAs in the same K order, only the operand delivery differs (ragged M and N, plain / GELU / gated
+    residual epilogues, both formats)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for c in ("2", "4"):
+        f = str(tmp_path / f"cl{c}.npz")
+        env = dict(os.environ, DMPQ_GEMM_CLUSTER=c)
+        subprocess.run([sys.executable, os.path.join(root, "scripts", "gemm_cluster_check.py"), f], env=env, check=True,
+                       timeout=600)
+        outs[c] = np.load(f)
+    assert sorted(outs["2"].files) == sorted(outs["4"].files) and len(outs["2"].files) == 18
+    for key in outs["2"].files:
+        assert np.array_equal(outs["2"][key], outs["4"][key]), key
